@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""bench.py -- input GB/s of PaREM DFA matching on B200 (BASELINE.json metric).
+
+One "step" = one pass of the whole hot path (boundaries + R_i, multi-start chunk
+simulation, map composition, result) over one input of the workload, through the C ABI
+(parem_match_async) with the input already resident in HBM.  Default workload (N=1):
+BASELINE.json configs[1] = cfg2, the 13-state DNA-motif KMP DFA over a 1 GiB seeded
+uniform input (larger than the 126 MB L2, so no flush is needed between steps).
+`--config k` selects another BASELINE config (k = 1..5).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config k] [--impl ours|reference]
+
+Multi-GPU (torchrun, one process per GPU): every rank matches its own independent input
+of the same config (weak scaling, no data-path collective -- the path partitions into
+independent problems); value = total bytes of all ranks / max-over-ranks device time.
+`--impl reference` times the oracle (single-threaded CPU walk, oracle/) on a bounded
+sample of the same workload: the reference arm of this tier.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "input GB/s of DFA matching on 1 B200 (device-timed) and % of HBM/lookup roofline"
+UNIT = "GB/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), float(j.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline(cfg, x, budget_s: float = 12.0, max_bytes: int = 256 << 20):
+    """The oracle as it stands: single-threaded C walk, on a bounded sample of the input."""
+    import oracle
+
+    sample = x[: min(x.size, max_bytes)]
+    reps, t_total = 0, 0.0
+    while t_total < budget_s and reps < 5:
+        t0 = time.perf_counter()
+        oracle.walk(cfg.table, cfg.start, cfg.accept, sample)
+        t_total += time.perf_counter() - t0
+        reps += 1
+    gbs = sample.size * reps / t_total / 1e9
+    return {"value": round(gbs, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {sample.size} bytes of the cfg{cfg.index} input x {reps} reps "
+                      f"({t_total:.1f} s, single thread)"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the box's host cores, K timed steps over bounded samples."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    import synth
+
+    cfg = synth.config(args.config)
+    sample_n = min(cfg.n, args.ref_sample)
+    x = cfg.make_input(sample_n)
+    for _ in range(args.warmup):
+        oracle.walk(cfg.table, cfg.start, cfg.accept, x[: min(x.size, 1 << 20)])
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.walk(cfg.table, cfg.start, cfg.accept, x)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    val = x.size * args.steps / tot / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (seeded, SURVEY §8(d) recipe)",
+        "config": {"workload": f"cfg{cfg.index}: {cfg.name}", "sample_bytes": int(x.size)},
+        "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"first {x.size} bytes of cfg{cfg.index}, {args.steps} steps"},
+        "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def latest_traffic(cfg_index: int):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", f"ncu_full_cfg{cfg_index}.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--boundary", default="snap", choices=["snap", "grid"])
+    ap.add_argument("--candidates", default="parem", choices=["parem", "enum"])
+    ap.add_argument("--chunk-len", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-micro", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=64 << 20)
+    ap.add_argument("--verify", action="store_true", help="bit-exact check against the oracle (full size)")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+
+    import paper_1412_1741_b200 as P
+    import synth
+
+    ws_, rank, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dist = None
+    if ws_ > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg = synth.config(args.config)
+    n = cfg.n
+    # rank-distinct input (weak scaling): offset the counter-based stream by rank * n
+    if cfg.input_kind == "markov":
+        x = synth.markov_bytes(n, cfg.input_seed + 1000 * rank) if rank else cfg.make_input()
+    else:
+        x = synth.uniform_symbols(n, cfg.A, cfg.input_seed, 0, rank * n)
+    xd = torch.from_numpy(x).to(f"cuda:{local}")
+    dfa = P.Dfa(cfg.table, cfg.start, cfg.accept)
+    opts = P.options(chunk_len=args.chunk_len, boundary=args.boundary, candidates=args.candidates)
+    plan = dfa.plan(n, opts)
+    info = dfa.info()
+    wsb = torch.empty(dfa.workspace_bytes(n, opts), dtype=torch.uint8, device=f"cuda:{local}")
+    res = torch.zeros(64, dtype=torch.uint8, device=f"cuda:{local}")
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        dfa.match_async(xd, wsb, res, opts, stream)
+    torch.cuda.synchronize()
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    per = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            per[i][0].record(stream)
+            dfa.match_async(xd, wsb, res, opts, stream)
+            per[i][1].record(stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t_ms = ev0.elapsed_time(ev1)
+    launch_ms = [a.elapsed_time(b) for a, b in per]
+    if dist:
+        tt = torch.tensor([t_ms], device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    r = P.MatchResult.from_bytes(res.cpu().numpy().tobytes()[:56])
+    assert r.status == 0, r
+
+    ms_per_step = t_ms / args.steps
+    total_bytes = n * ws_ * args.steps
+    value = total_bytes / (t_ms / 1e3) / 1e9
+
+    # ---- e2e: the same metric through parem_match_host (pinned host buffer, H2D + D2H inside)
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.from_numpy(x).pin_memory()
+        dfa.match_host(hx)
+        torch.cuda.synchronize()
+        e_steps = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            rh = dfa.match_host(hx)
+        t_e2e = (time.perf_counter() - t0) / e_steps
+        if dist:
+            tt = torch.tensor([t_e2e], device=f"cuda:{local}")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        assert (rh.final_state, rh.match_count) == (r.final_state, r.match_count)
+        e2e = {"value": round(n * ws_ / t_e2e / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": int(n),
+               "d2h_bytes_per_step": 56, "ms_per_step": round(1e3 * t_e2e, 3), "api": "parem_match_host"}
+
+    # ---- in-run roofline micro-benchmarks (denominators measured in the same run)
+    hbm_peak, sm_mhz_max, peak_src = peaks()
+    micro = {}
+    if not args.no_micro:
+        sink = torch.zeros(4, dtype=torch.int32, device=f"cuda:{local}")
+        L = P.lib()
+        import ctypes as C
+
+        ms = L.parem_bench_read_stream(C.c_void_p(xd.data_ptr()), n, C.c_void_p(sink.data_ptr()), 5,
+                                       C.c_void_p(stream.cuda_stream))
+        micro["read_stream_gbs"] = round(n / (ms * 1e-3) / 1e9, 1) if ms > 0 else None
+        rng = np.random.default_rng(0)
+        for where, nm, ent in ((2, "smem_lane_private", 1 << 10), (0, "smem_random_16KiB", 1 << 13),
+                               (1, "l2_random_2MiB", 1 << 20)):
+            tabx = torch.from_numpy(rng.integers(0, 1 << 16, ent).astype(np.uint16)).to(xd.device)
+            lk = C.c_uint64()
+            ms = L.parem_bench_gather(where, C.c_void_p(tabx.data_ptr()), ent, 256, C.c_void_p(sink.data_ptr()),
+                                      C.byref(lk), 3, C.c_void_p(stream.cuda_stream))
+            micro[f"gather_{nm}_lookups_per_s"] = float(f"{lk.value / (ms * 1e-3):.4g}") if ms > 0 else None
+        torch.cuda.synchronize()
+
+    clocks = clk.summary()
+    sm_clk = clocks["sm_mhz"] or sm_mhz_max
+    kernel_ms = statistics.median(launch_ms)
+    W_exec = r.route_steps / n
+    lookups_per_s = r.route_steps / (kernel_ms * 1e-3)
+    smem_peak = 148 * 32 * sm_mhz_max * 1e6     # architectural LDS lookups/s at max clock
+    if info["table_class"] == 1 and cfg.A <= 4:
+        bound = {"bound": "hbm", "achieved": round(n / (kernel_ms * 1e-3) / 1e9, 1), "peak": hbm_peak,
+                 "unit": "GB/s"}
+    elif info["table_class"] in (1, 2):
+        bound = {"bound": "smem_lookup", "achieved": float(f"{lookups_per_s / 1e12:.4g}"),
+                 "peak": float(f"{smem_peak / 1e12:.4g}"), "unit": "Tlookup/s"}
+    else:
+        bound = {"bound": "l2_lookup", "achieved": float(f"{lookups_per_s / 1e12:.4g}"),
+                 "peak": float(f"{smem_peak / 1e12:.4g}"), "unit": "Tlookup/s"}
+    bound["frac"] = round(bound["achieved"] / bound["peak"], 4)
+    bound["traffic"] = latest_traffic(cfg.index)
+    bound["peak_source"] = peak_src if bound["bound"] == "hbm" else "148 SMs x 32 lookups/clk x sm_max_mhz"
+    bound["kernel_ms"] = round(kernel_ms, 4)
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws_, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (seeded, SURVEY §8(d) recipe; no public dataset in the paper)",
+        "config": {"workload": f"cfg{cfg.index}: {cfg.name}", "n_bytes": n, "states": cfg.Q, "alphabet": cfg.A,
+                   "boundary": args.boundary, "candidates": args.candidates, "kernel": plan["kernel"],
+                   "chunks": plan["num_chunks"], "chunk_len": plan["chunk_len"], "grid": plan["grid_blocks"],
+                   "block": plan["block_threads"], "slots": plan["slots"],
+                   "l2": "input larger than L2 (no flush needed)" if n > (126 << 20) else "input fits L2 (warm)",
+                   "parallelism": f"weak x{ws_} (independent inputs per rank)"},
+        "roofline": bound,
+        "W_grid": round(info["sum_L"] / cfg.A, 4), "W_exec": round(W_exec, 4),
+        "result": {"final_state": r.final_state, "accepted": r.accepted, "match_count": r.match_count,
+                   "routes": r.routes},
+        "gpu_launches": args.steps,
+        "clocks": clocks,
+        "e2e": e2e,
+        "micro": micro,
+    }
+    if not args.no_cpu_baseline and rank == 0 and ws_ == 1:
+        line["cpu_baseline"] = cpu_baseline(cfg, x)
+    if args.verify and rank == 0:
+        import oracle
+
+        ref = oracle.walk(cfg.table, cfg.start, cfg.accept, x)
+        line["verified"] = (ref.final_state, ref.accepted, ref.match_count) == (r.final_state, r.accepted, r.match_count)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    dfa.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,194 @@
+/*
+ * parem.h -- C ABI of the B200-native PaREM hot path: chunked, speculative DFA matching.
+ *
+ * Method (PAPER.md = /root/reference/PAPER.md, cited "P:line"):
+ *   * DFA (Q, Sigma, delta, q0, F); a string is accepted iff the last state is in F.
+ *   * The input T is split into p chunks (domain decomposition, Alg. 1 lines 3-4
+ *     P:81-82).  Chunk i >= 1 is run from every state of R_i = S(c_first) n L(c_last)
+ *     (P:67): S(c) = states with a transition on the chunk's first symbol,
+ *     L(c) = distinct destinations on the previous chunk's last symbol (reading C1).
+ *     Chunk 0 starts from q0 only.
+ *   * Each route counts the positions whose destination state is in F (Alg. 1 P:104-107,
+ *     reading C3/C4: per-route counts), giving a per-chunk map start -> (end, hits).
+ *   * The maps are joined by start state (reading C5) -- an associative function
+ *     composition -- into (final state, accept flag, match count).
+ *
+ * Result semantics (identical to the sequential walk, readings C3, C9, C11, C12 of DESIGN.md):
+ *   final_state  = q_n, or PAREM_DEAD if a missing transition was taken;
+ *   accepted     = final_state in F (0 if DEAD);
+ *   match_count  = #{k in [1, n] : q_k in F} (u64; the start state is never counted;
+ *                  hits before a death are kept);
+ *   n = 0        -> (q0, q0 in F, 0);
+ *   any byte >= alphabet_size -> status PAREM_ESYMBOL, bad_offset = smallest such offset
+ *                  (all n bytes are checked, regardless of death); other fields undefined.
+ *
+ * Threading: a parem_dfa handle is immutable after creation; concurrent matches on
+ * different streams are safe as long as each in-flight call has its own workspace.
+ * No function aborts or exits; errors are status codes with a thread-local message.
+ */
+#ifndef PAREM_H
+#define PAREM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---- */
+#define PAREM_OK 0
+#define PAREM_EINVAL (-1)     /* bad argument (host-detectable)                          */
+#define PAREM_ESYMBOL (-2)    /* input byte >= alphabet_size (device-detected)           */
+#define PAREM_ECUDA (-3)      /* CUDA runtime error (message via parem_last_error)       */
+#define PAREM_ENOMEM (-4)     /* allocation failed / workspace too small                 */
+#define PAREM_EINTERNAL (-5)  /* internal invariant violated (e.g. speculation unsound)  */
+
+/* Output sentinel for a dead walk.  On INPUT, a DEAD (missing) transition is the
+ * all-ones value of the table element width (0xFFFF for uint16, 0xFFFFFFFF for uint32);
+ * the paper treats tables as possibly sparse. */
+#define PAREM_DEAD 0xFFFFFFFFu
+
+/* boundary_policy */
+#define PAREM_BOUNDARY_GRID 0u   /* b_i = i * chunk_len, remainder to the last chunk (C7)   */
+#define PAREM_BOUNDARY_SNAP 1u   /* planner: move b_i forward (<= window) to minimise |L(T[b_i-1])| */
+/* candidates */
+#define PAREM_CANDIDATES_PAREM 0u  /* R_i = S n L (the paper's rule)                        */
+#define PAREM_CANDIDATES_ENUM 1u   /* every chunk i >= 1 starts from all of Q (Enum) */
+
+/* Result of one match (56 bytes).  routes = sum_i |R_i| ("calculations"; with
+ * |R_0| = 1), route_steps = sum_i |R_i| * len_i (candidate-steps, the lookup roofline's
+ * work), num_chunks = p. */
+typedef struct parem_result {
+    uint64_t match_count;
+    uint32_t final_state;
+    uint32_t accepted;
+    uint64_t bad_offset;
+    uint64_t num_chunks;
+    uint64_t routes;
+    uint64_t route_steps;
+    int32_t status;
+    uint32_t reserved;
+} parem_result;
+
+/* Options (NULL = defaults: planner-chosen chunk length, SNAP, PaREM candidates).
+ * chunk_len forces the nominal chunk length (bytes, >= 1): p = max(1, floor(n / chunk_len))
+ * chunks; with GRID the remainder goes to the last chunk.  Results are independent of all
+ * options (only the stats routes/route_steps/num_chunks change). */
+typedef struct parem_options {
+    uint64_t chunk_len;
+    uint32_t boundary_policy;
+    uint32_t candidates;
+    uint32_t kernel;       /* 0 = auto; 1 = tiny (thread per chunk); 2 = lanes (CTA per chunk) */
+    uint32_t reserved[3];
+} parem_options;
+
+typedef struct parem_dfa parem_dfa;
+
+/* Create a DFA handle (P:58 quintuple; the table is the paper's adjacency matrix Tt,
+ * P:76).
+ *   num_states     Q >= 1 (Q <= 65535 for 2-byte tables).
+ *   alphabet_size  A in [1, 256]; symbols are raw byte values 0..A-1 (mapping characters
+ *                  to symbols is the caller's job).
+ *   table          host pointer, row-major Q x A, table[s*A + c] = delta(s, c), elements of
+ *                  elem_bytes (2 or 4) bytes; an entry is < Q or DEAD (all-ones).
+ *   start_state    q0 < Q.
+ *   accept_bitmap  host pointer, ceil(Q/8) bytes, LSB-first: s in F iff bit (s & 7) of byte s>>3.
+ * The library copies table and bitmap (the caller keeps ownership) and uploads device
+ * copies to the current CUDA device.  Returns PAREM_EINVAL on a bad argument, PAREM_ECUDA /
+ * PAREM_ENOMEM on device failure; *out is set only on success. */
+int parem_dfa_create(uint32_t num_states, uint32_t alphabet_size, const void* table, uint32_t elem_bytes,
+                     uint32_t start_state, const uint8_t* accept_bitmap, parem_dfa** out);
+
+/* Destroy a handle.  The caller guarantees no in-flight match uses it.  NULL is a no-op. */
+int parem_dfa_destroy(parem_dfa* dfa);
+
+/* Workspace bytes needed by parem_match_async for an n-byte input with these options
+ * (0 on bad arguments).  The caller allocates device memory of at least this size
+ * (e.g. torch.empty(ws, dtype=torch.uint8, device="cuda")); one per in-flight call. */
+size_t parem_workspace_bytes(const parem_dfa* dfa, uint64_t n, const parem_options* opts);
+
+/* Enqueue one match on `stream` (graph-capturable; no host synchronisation).
+ *   d_input    device pointer to n bytes, any alignment, caller-owned, valid until the
+ *              stream work completes.
+ *   d_ws       device workspace of ws_bytes >= parem_workspace_bytes(...).
+ *   d_result   device pointer to one parem_result, written by the last kernel.
+ * Host-detectable errors return immediately (nothing enqueued); device-side errors
+ * (PAREM_ESYMBOL with the smallest bad_offset) land in d_result->status. */
+int parem_match_async(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, void* d_ws, size_t ws_bytes,
+                      const parem_options* opts, parem_result* d_result, void* stream /* cudaStream_t */);
+
+/* Like parem_match_async, but the walk continues from a previous segment's result:
+ * the start state is d_carry->final_state (PAREM_DEAD stays dead), counts add to
+ * d_carry->match_count and bad offsets are reported as offset_base + local offset
+ * (an earlier ESYMBOL in d_carry wins).  d_carry may equal d_result.  This is the
+ * associativity of the composition exposed at the ABI: segments can be streamed. */
+int parem_match_continue_async(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, uint64_t offset_base,
+                               void* d_ws, size_t ws_bytes, const parem_options* opts,
+                               const parem_result* d_carry, parem_result* d_result, void* stream);
+
+/* Convenience: internal workspace, D2H copy of the result and a stream sync.
+ * Returns the result's status (PAREM_OK, PAREM_ESYMBOL, ...). */
+int parem_match(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, const parem_options* opts,
+                parem_result* h_result, void* stream);
+
+/* End to end from HOST memory: pipelines host->device copies of h_input (pinned memory
+ * recommended) in segments with matching (parem_match_continue_async) on `stream`, then
+ * copies the result back and synchronises.  Internal device buffers are allocated per
+ * call.  Returns the result's status. */
+int parem_match_host(const parem_dfa* dfa, const uint8_t* h_input, uint64_t n, const parem_options* opts,
+                     parem_result* h_result, void* stream);
+
+/* Introspection (tests, bench, DESIGN.md numbers). */
+typedef struct parem_dfa_info {
+    uint32_t num_states;      /* Q as given                                  */
+    uint32_t internal_states; /* Q + 1 if a DEAD sink was added, else Q      */
+    uint32_t alphabet_size;
+    uint32_t has_sink;
+    uint32_t min_L;           /* min_c |L(c)| over c < A                     */
+    uint32_t max_L;           /* max_c |L(c)|                                */
+    uint64_t sum_L;           /* sum_c |L(c)|                                */
+    uint32_t start_state;
+    uint32_t table_class;     /* 1 = tiny (<= 32 states), 2 = lanes/smem, 3 = lanes/L2 */
+    uint64_t device_bytes;    /* device memory held by the handle            */
+} parem_dfa_info;
+int parem_dfa_get_info(const parem_dfa* dfa, parem_dfa_info* info);
+
+typedef struct parem_plan_info {
+    uint32_t kernel;          /* 1 tiny, 2 lanes                                  */
+    uint32_t block_threads;
+    uint64_t grid_blocks;
+    uint64_t num_chunks;      /* p                                                */
+    uint64_t chunk_len;       /* nominal chunk length                             */
+    uint32_t boundary_policy;
+    uint32_t candidates;
+    uint32_t slots;           /* candidate registers/lanes per chunk per pass     */
+    uint32_t symbols_per_lookup;
+    size_t smem_bytes;
+    size_t workspace_bytes;
+    uint32_t snap_window;
+    uint32_t reserved;
+} parem_plan_info;
+int parem_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, parem_plan_info* out);
+
+/* Message of the last error on this thread ("" if none). */
+const char* parem_last_error(void);
+
+/* Version string. */
+const char* parem_version(void);
+
+/* ---- roofline micro-benchmarks (bench.py; not part of the matching path) ----
+ * Each returns the device time in milliseconds of `reps` back-to-back launches measured
+ * with CUDA events on `stream` (or a negative status).
+ *   read_stream: 16-B vector loads over n bytes, grid-stride, reduced to *d_sink.
+ *   gather:      every thread performs `steps` dependent random lookups into a table of
+ *                table_bytes (uint16 entries) held in shared memory (where=0) or global /
+ *                L2 (where=1); lookups_out = total lookups per launch. */
+float parem_bench_read_stream(const uint8_t* d_input, uint64_t n, uint32_t* d_sink, int reps, void* stream);
+float parem_bench_gather(uint32_t where, const uint16_t* d_table, uint32_t table_entries, uint32_t steps,
+                         uint32_t* d_sink, uint64_t* lookups_out, int reps, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAREM_H */

@@ -1,0 +1,212 @@
+"""B200-native PaREM hot path: chunked, speculative DFA matching (arXiv 1412.1741).
+
+Thin Python binding over the C ABI (include/parem.h, libparem.so).  Every step of the
+path runs in the library's sm_100a kernels; this module only marshals arguments.
+PyTorch supplies device memory and the current CUDA stream.  There is no CPU fallback:
+matching a non-CUDA tensor, or importing without the built library, raises.
+
+    import numpy as np, torch
+    from paper_1412_1741_b200 import Dfa
+    dfa = Dfa(table_u16_or_u32, start=0, accept=bool_array)
+    final, accepted, count = dfa.match(torch_uint8_cuda_tensor)[:3]
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import NamedTuple
+
+import numpy as np
+
+from . import _abi
+from ._abi import (BOUNDARY_GRID, BOUNDARY_SNAP, CANDIDATES_ENUM, CANDIDATES_PAREM, KERNEL_AUTO, KERNEL_LANES,
+                   KERNEL_TINY, PAREM_DEAD, PAREM_EINVAL, PAREM_ESYMBOL, PAREM_OK)
+
+__all__ = ["Dfa", "MatchResult", "ParemError", "options", "PAREM_DEAD", "PAREM_OK", "PAREM_ESYMBOL",
+           "PAREM_EINVAL", "lib"]
+
+
+def lib():
+    return _abi.load()
+
+
+class ParemError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"parem status {status}: {msg}")
+        self.status = status
+
+
+class MatchResult(NamedTuple):
+    final_state: int          # PAREM_DEAD (0xFFFFFFFF) if the walk died
+    accepted: bool
+    match_count: int
+    status: int
+    bad_offset: int
+    num_chunks: int
+    routes: int               # sum |R_i|   ("calculations")
+    route_steps: int          # sum |R_i| * len_i
+
+    @staticmethod
+    def from_struct(r: _abi.parem_result) -> "MatchResult":
+        return MatchResult(r.final_state, bool(r.accepted), r.match_count, r.status, r.bad_offset, r.num_chunks,
+                           r.routes, r.route_steps)
+
+    @staticmethod
+    def from_bytes(b: bytes) -> "MatchResult":
+        return MatchResult.from_struct(_abi.parem_result.from_buffer_copy(b))
+
+
+_POLICY = {"grid": BOUNDARY_GRID, "snap": BOUNDARY_SNAP}
+_CAND = {"parem": CANDIDATES_PAREM, "enum": CANDIDATES_ENUM}
+_KERNEL = {"auto": KERNEL_AUTO, "tiny": KERNEL_TINY, "lanes": KERNEL_LANES}
+
+
+def options(chunk_len: int = 0, boundary: str = "snap", candidates: str = "parem", kernel: str = "auto"):
+    o = _abi.parem_options()
+    o.chunk_len = int(chunk_len)
+    o.boundary_policy = _POLICY[boundary]
+    o.candidates = _CAND[candidates]
+    o.kernel = _KERNEL[kernel]
+    return o
+
+
+def _err(L, status: int):
+    raise ParemError(status, L.parem_last_error().decode(errors="replace"))
+
+
+def _cuda_u8(x):
+    import torch
+
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise TypeError("input must be a CUDA torch.Tensor (no CPU fallback)")
+    if x.dtype != torch.uint8 or not x.is_contiguous():
+        raise TypeError("input must be a contiguous uint8 tensor")
+    return x
+
+
+def _stream(stream):
+    import torch
+
+    if stream is None:
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if hasattr(stream, "cuda_stream"):
+        return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(int(stream))
+
+
+class Dfa:
+    """A DFA handle on the current CUDA device (parem_dfa_create).
+
+    table  -- (Q, A) uint16/uint32 array, table[s, c] = delta(s, c); all-ones = DEAD.
+    start  -- q0.
+    accept -- bool[Q] (or an LSB-first bitmap of ceil(Q/8) bytes).
+    """
+
+    def __init__(self, table, start: int, accept):
+        self._L = lib()
+        t = np.ascontiguousarray(table)
+        if t.ndim != 2 or t.dtype not in (np.uint16, np.uint32):
+            raise TypeError("table must be a 2-D uint16/uint32 array")
+        Q, A = t.shape
+        a = np.asarray(accept)
+        bm = np.packbits(a.astype(bool), bitorder="little") if a.dtype == bool else np.ascontiguousarray(a, np.uint8)
+        if bm.size < (Q + 7) // 8:
+            raise ValueError("accept bitmap too short")
+        h = C.c_void_p()
+        st = self._L.parem_dfa_create(Q, A, t.ctypes.data, t.itemsize, int(start), bm.ctypes.data, C.byref(h))
+        if st != PAREM_OK:
+            _err(self._L, st)
+        self._h = h
+        self.Q, self.A, self.start = Q, A, int(start)
+
+    # -- lifetime --
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.parem_dfa_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- introspection --
+    def info(self) -> dict:
+        i = _abi.parem_dfa_info()
+        st = self._L.parem_dfa_get_info(self._h, C.byref(i))
+        if st != PAREM_OK:
+            _err(self._L, st)
+        return {f: getattr(i, f) for f, _ in i._fields_}
+
+    def plan(self, n: int, opts=None) -> dict:
+        p = _abi.parem_plan_info()
+        st = self._L.parem_plan(self._h, n, C.byref(opts) if opts is not None else None, C.byref(p))
+        if st != PAREM_OK:
+            _err(self._L, st)
+        return {f: getattr(p, f) for f, _ in p._fields_ if f != "reserved"}
+
+    def workspace_bytes(self, n: int, opts=None) -> int:
+        ws = self._L.parem_workspace_bytes(self._h, n, C.byref(opts) if opts is not None else None)
+        if ws == 0:
+            _err(self._L, PAREM_EINVAL)
+        return ws
+
+    # -- matching --
+    def match(self, x, opts=None, stream=None, **kw) -> MatchResult:
+        """Synchronous match of a CUDA uint8 tensor (parem_match)."""
+        x = _cuda_u8(x)
+        opts = opts if opts is not None else (options(**kw) if kw else None)
+        r = _abi.parem_result()
+        st = self._L.parem_match(self._h, C.c_void_p(x.data_ptr()), x.numel(),
+                                 C.byref(opts) if opts is not None else None, C.byref(r), _stream(stream))
+        if st not in (PAREM_OK, PAREM_ESYMBOL):
+            _err(self._L, st)
+        return MatchResult.from_struct(r)
+
+    def match_async(self, x, ws, result, opts=None, stream=None, n: int | None = None) -> None:
+        """Enqueue parem_match_async; ``ws`` is a CUDA uint8 workspace tensor and ``result`` a
+        CUDA uint8 tensor of >= 56 bytes that receives the parem_result."""
+        x = _cuda_u8(x)
+        n = x.numel() if n is None else n
+        st = self._L.parem_match_async(self._h, C.c_void_p(x.data_ptr()), n, C.c_void_p(ws.data_ptr()), ws.numel(),
+                                       C.byref(opts) if opts is not None else None, C.c_void_p(result.data_ptr()),
+                                       _stream(stream))
+        if st != PAREM_OK:
+            _err(self._L, st)
+
+    def match_continue_async(self, x, offset_base: int, ws, carry, result, opts=None, stream=None) -> None:
+        x = _cuda_u8(x)
+        st = self._L.parem_match_continue_async(
+            self._h, C.c_void_p(x.data_ptr()), x.numel(), offset_base, C.c_void_p(ws.data_ptr()), ws.numel(),
+            C.byref(opts) if opts is not None else None, C.c_void_p(carry.data_ptr()) if carry is not None else None,
+            C.c_void_p(result.data_ptr()), _stream(stream))
+        if st != PAREM_OK:
+            _err(self._L, st)
+
+    def match_host(self, x, opts=None, stream=None) -> MatchResult:
+        """End-to-end match of a HOST buffer (numpy uint8 array or CPU torch tensor; pinned
+        memory recommended): parem_match_host pipelines H2D copies with matching."""
+        try:
+            import torch
+
+            if isinstance(x, torch.Tensor):
+                if x.is_cuda or x.dtype != torch.uint8 or not x.is_contiguous():
+                    raise TypeError("host input must be a contiguous CPU uint8 tensor")
+                ptr, n = x.data_ptr(), x.numel()
+            else:
+                raise ImportError
+        except ImportError:
+            a = np.ascontiguousarray(x, dtype=np.uint8)
+            ptr, n = a.ctypes.data, a.size
+        r = _abi.parem_result()
+        st = self._L.parem_match_host(self._h, C.c_void_p(ptr), n, C.byref(opts) if opts is not None else None,
+                                      C.byref(r), _stream(stream))
+        if st not in (PAREM_OK, PAREM_ESYMBOL):
+            _err(self._L, st)
+        return MatchResult.from_struct(r)

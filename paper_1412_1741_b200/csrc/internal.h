@@ -1,0 +1,113 @@
+// internal.h -- internal types of the PaREM B200 library (not part of the ABI).
+//
+// Data layout in HBM / shared memory:
+//   * the caller's table is turned into a COMPLETE internal table over Qp = Q (+1 sink if
+//     any entry is DEAD): DEAD -> sink, sink -> sink, sink not accepting (reading C9);
+//   * L(c) lists (sorted, over the original Q, DEAD excluded: P:67) for every
+//     symbol, plus list A = all of Q (Enum candidates);
+//   * tiny class (Qp <= 32): tab1[s][c] = dest | acc(dest) << 15 (u16) and, for A <= 4,
+//     the 4-bit-group stride table stride[s][g] = dest << 11 | hits << 28 (g packs
+//     4/B symbols of B bits, earliest symbol in the low bits);
+//   * lanes class (Qp > 32): symbol-major tabL[c][s] over Apad x Qpad (powers of two),
+//     entry = dest * ES | acc(dest) << (8*ES - 1) with ES = 2 (u16) or 4 (u32) bytes, so
+//     the next byte offset is (entry & SMASK) | (c << SHC) -- one LOP3 per lookup.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include <vector>
+
+#include "parem.h"
+
+namespace parem {
+
+constexpr uint32_t kTinyMaxStates = 32;   // dense per-chunk maps live in one warp
+constexpr uint32_t kTinyThreads = 256;    // threads (= chunks) per CTA, tiny kernel
+constexpr uint32_t kTinyMaxA = 256;
+constexpr uint32_t kKernelTrivial = 0, kKernelTiny = 1, kKernelLanes = 2;
+
+struct DevDfa {                // POD, passed by value to every kernel
+    uint32_t Q, Qp, Qpad, A;
+    uint32_t Apad, sink, start, has_sink;
+    uint32_t log2Qpad, Lmin, Lmax, sym_bits;   // sym_bits: 0 (no stride table), 1, 2
+    uint32_t lanes_u32, Lsum_all, pad0, pad1;  // Lsum_all = total list entries incl. list A
+    const uint8_t* acc;        // [Qp] accept flag per internal state
+    const uint32_t* Loff;      // [A+1]
+    const uint32_t* Lcnt;      // [A+1]
+    const uint32_t* Llist;     // concatenated lists
+    const uint32_t* Rcnt;      // [A*A] |L(a) n S(b)| (partial tables only), else nullptr
+    const uint16_t* tab1;      // tiny: [Qp][A]
+    const uint32_t* stride;    // tiny: [Qp][16]
+    const void* lanes_tab;     // lanes: [Apad][Qpad]
+};
+
+struct WsHeader {              // first 64 bytes of every workspace (memset to 0 per call)
+    unsigned int done;         // CTAs finished (last-CTA detection)
+    unsigned int pad;
+    unsigned long long bad_inv;  // ~(smallest bad local offset); 0 = none
+    unsigned long long routes;   // sum |R_i|
+    unsigned long long steps;    // sum |R_i| * len_i
+    unsigned long long pad2[4];
+};
+static_assert(sizeof(WsHeader) == 64, "header");
+
+struct MatchParams {
+    DevDfa d;
+    const uint8_t* in;
+    uint64_t n;
+    uint64_t L;                // nominal chunk length
+    uint64_t p;                // number of chunks
+    uint32_t policy, cand, win, slots;
+    uint64_t offset_base;
+    const parem_result* carry; // may be null
+    parem_result* result;
+    WsHeader* hdr;
+    void* maps;                // tiny: tile maps [grid][Qpad] u64; lanes: ends [p][Qpad] u32 + hits
+    uint32_t* map_hits;        // lanes only
+};
+
+struct Plan {
+    uint32_t kernel;
+    uint32_t threads;
+    uint64_t grid;
+    uint64_t p, L;
+    uint32_t policy, cand, slots, U;
+    uint32_t sym_per_lookup;
+    uint32_t win;
+    uint32_t smem_tab;       // lanes: table staged in shared memory
+    size_t smem;
+    size_t ws;
+    size_t off_maps, off_hits;
+};
+
+}  // namespace parem
+
+struct parem_dfa {
+    parem::DevDfa dev;
+    uint32_t Q, A, start, eb;
+    uint32_t Lmin, Lmax;
+    uint64_t Lsum;
+    uint32_t table_class;
+    int device;
+    void* dev_block;
+    size_t dev_bytes;
+    int num_sms;
+};
+
+namespace parem {
+// host side (dfa.cpp / planner.cpp)
+void set_error(const char* fmt, ...);
+int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan* plan);
+// device side (kernels_*.cu)
+int launch_tiny(const Plan& plan, const MatchParams& P, cudaStream_t s);
+int launch_lanes(const Plan& plan, const MatchParams& P, cudaStream_t s);
+int launch_trivial(const MatchParams& P, cudaStream_t s);
+int tiny_blocks_per_sm(uint32_t K, uint32_t B, size_t smem);
+size_t tiny_smem_bytes(const DevDfa& d, uint32_t B);
+size_t lanes_smem_bytes(const DevDfa& d, bool smem_tab);
+int lanes_blocks_per_sm(uint32_t U, bool smem_tab, bool u32, uint32_t threads, size_t smem);
+uint32_t tiny_round_slots(uint32_t k);
+uint32_t lanes_round_u(uint32_t u);
+}  // namespace parem

@@ -1,0 +1,146 @@
+// planner.cpp -- the chunk-size / candidate-set planner (north_star
+// subsystem (3)).  It trades redundant work against parallelism:
+//   * the paper splits into p = #processing units chunks of T.length/p;
+//     on a GPU "processing units" are register slots / lanes, so the default is ONE wave
+//     of resident CTAs (every thread/CTA gets exactly one chunk; no tail effect);
+//   * redundant work is sum_i (|R_i| - 1) * len_i; the SNAP policy moves each nominal
+//     boundary forward (<= win bytes) to a position whose preceding symbol minimises
+//     |L(c)|, so the tiny kernel can size its register slots for min_c |L(c)| instead of
+//     max_c |L(c)| (W_exec <= W_grid; results are partition-invariant);
+//   * slots (registers per thread, or lanes per CTA) are sized for the expected |R_i|;
+//     a chunk with more candidates runs extra passes over its bytes.
+#include <string.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "internal.h"
+
+namespace parem {
+
+static int cached_bps(int kind, uint32_t a, uint32_t b, uint32_t c, uint32_t threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, uint32_t, uint32_t, uint32_t, uint32_t, size_t, int>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto key = std::make_tuple(kind, a, b, c, threads, smem, dev);
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    int v = kind == 1 ? tiny_blocks_per_sm(a, b, smem) : lanes_blocks_per_sm(a, b != 0, c != 0, threads, smem);
+    std::lock_guard<std::mutex> g(mu);
+    cache[key] = v;
+    return v;
+}
+
+static uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan* plan) {
+    memset(plan, 0, sizeof(*plan));
+    if (!dfa) { set_error("null dfa"); return PAREM_EINVAL; }
+    const DevDfa& d = dfa->dev;
+    const uint32_t policy = opts ? opts->boundary_policy : PAREM_BOUNDARY_SNAP;
+    const uint32_t cand = opts ? opts->candidates : PAREM_CANDIDATES_PAREM;
+    const uint32_t kreq = opts ? opts->kernel : 0;
+    const uint64_t forced = opts ? opts->chunk_len : 0;
+    if (policy > PAREM_BOUNDARY_SNAP) { set_error("bad boundary_policy %u", policy); return PAREM_EINVAL; }
+    if (cand > PAREM_CANDIDATES_ENUM) { set_error("bad candidates %u", cand); return PAREM_EINVAL; }
+    if (kreq > kKernelLanes) { set_error("bad kernel %u", kreq); return PAREM_EINVAL; }
+    plan->policy = policy;
+    plan->cand = cand;
+    if (n == 0) {
+        plan->kernel = kKernelTrivial;
+        plan->threads = 32;
+        plan->grid = 1;
+        plan->ws = 256;
+        return PAREM_OK;
+    }
+    uint32_t kernel = kreq ? kreq : (d.Qp <= kTinyMaxStates ? kKernelTiny : kKernelLanes);
+    if (kernel == kKernelTiny && d.Qp > kTinyMaxStates) {
+        set_error("tiny kernel needs <= %u internal states (have %u)", kTinyMaxStates, d.Qp);
+        return PAREM_EINVAL;
+    }
+    if (kernel == kKernelLanes && !d.lanes_tab) {
+        set_error("lanes kernel needs a lanes table (DFA has <= %u states)", kTinyMaxStates);
+        return PAREM_EINVAL;
+    }
+    plan->kernel = kernel;
+    const int sms = dfa->num_sms > 0 ? dfa->num_sms : 148;
+
+    if (kernel == kKernelTiny) {
+        const uint32_t B = d.sym_bits;
+        uint32_t need = cand == PAREM_CANDIDATES_ENUM ? d.Q : (policy == PAREM_BOUNDARY_SNAP ? d.Lmin : d.Lmax);
+        if (need < 1) need = 1;
+        const uint32_t K = tiny_round_slots(need);
+        const size_t smem = tiny_smem_bytes(d, B);
+        int bps = cached_bps(1, K, B, 0, kTinyThreads, smem);
+        if (bps <= 0) { set_error("tiny kernel does not fit (smem %zu)", smem); return PAREM_EINVAL; }
+        uint64_t L;
+        if (forced) L = forced;
+        else {
+            const uint64_t target = (uint64_t)sms * bps * kTinyThreads;
+            L = ceil_div(n, target);
+            L = (L + 15) & ~15ull;
+            if (L < 256) L = 256;
+        }
+        if (L > (1ull << 30)) L = 1ull << 30;
+        const uint64_t p = n / L ? n / L : 1;
+        plan->threads = kTinyThreads;
+        plan->grid = ceil_div(p, kTinyThreads);
+        plan->p = p;
+        plan->L = L;
+        plan->slots = K;
+        plan->U = 1;
+        plan->sym_per_lookup = B ? 4 / B : 1;
+        plan->win = (policy == PAREM_BOUNDARY_SNAP && L > 1) ? (uint32_t)(L - 1 < 64 ? L - 1 : 64) : 0;
+        plan->smem = smem;
+        plan->off_maps = 256;
+        plan->ws = al256(plan->off_maps + plan->grid * d.Qpad * 8);
+        if (plan->grid > 0x7FFFFFFFull) { set_error("too many chunks"); return PAREM_EINVAL; }
+        return PAREM_OK;
+    }
+
+    // lanes
+    const size_t ES = d.lanes_u32 ? 4 : 2;
+    const size_t tab_bytes = (size_t)d.Apad * d.Qpad * ES;
+    const bool smem_tab = tab_bytes <= (size_t)160 * 1024;
+    uint32_t S = cand == PAREM_CANDIDATES_ENUM ? d.Q : d.Lmax;
+    if (S < 1) S = 1;
+    uint32_t U = S <= 64 ? 1 : S <= 2048 ? 2 : S <= 4096 ? 4 : 8;
+    uint64_t T = 32 * ceil_div(S, 32ull * U);
+    if (T > 1024) T = 1024;
+    const size_t smem = lanes_smem_bytes(d, smem_tab);
+    int bps = cached_bps(2, U, smem_tab, d.lanes_u32, (uint32_t)T, smem);
+    if (bps <= 0) { set_error("lanes kernel does not fit (smem %zu, threads %llu)", smem, (unsigned long long)T); return PAREM_EINVAL; }
+    uint64_t L;
+    if (forced) L = forced;
+    else {
+        const uint64_t target = (uint64_t)sms * bps;
+        L = ceil_div(n, target);
+        L = (L + 15) & ~15ull;
+        if (L < 4096) L = 4096;
+    }
+    if (L > (1ull << 30)) L = 1ull << 30;
+    const uint64_t p = n / L ? n / L : 1;
+    plan->threads = (uint32_t)T;
+    plan->grid = p;
+    plan->p = p;
+    plan->L = L;
+    plan->slots = (uint32_t)(T * U);
+    plan->U = U;
+    plan->sym_per_lookup = 1;
+    plan->win = (policy == PAREM_BOUNDARY_SNAP && L > 1) ? (uint32_t)(L - 1 < 4096 ? L - 1 : 4096) : 0;
+    plan->smem_tab = smem_tab;
+    plan->smem = smem;
+    plan->off_maps = 256;
+    plan->off_hits = al256(plan->off_maps + p * d.Qpad * 4);
+    plan->ws = al256(plan->off_hits + p * d.Qpad * 4);
+    if (p > 0x7FFFFFFFull) { set_error("too many chunks"); return PAREM_EINVAL; }
+    return PAREM_OK;
+}
+
+}  // namespace parem

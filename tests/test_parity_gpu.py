@@ -1,0 +1,254 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element
+on the same seeded inputs -- final state, accept flag and match count bit-exact (integer
+path, BASELINE north_star), stats against the paper's route rule (oracle.route_stats)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_mod(cuda_device):
+    import torch
+
+    return torch
+
+
+@pytest.fixture(scope="module")
+def parem(cuda_device):
+    import paper_1412_1741_b200 as P
+
+    P.lib()
+    return P
+
+
+def to_dev(torch, x, offset=0):
+    """Copy bytes to the device; ``offset`` > 0 yields a deliberately unaligned view."""
+    buf = torch.empty(x.size + offset + 16, dtype=torch.uint8, device="cuda")
+    view = buf[offset:offset + x.size]
+    if x.size:
+        view.copy_(torch.from_numpy(np.ascontiguousarray(x)))
+    return view
+
+
+def check(parem, torch, table, start, acc, x, opts=None, offset=0, expect=None):
+    ref = oracle.walk(table, start, acc, x)
+    with parem.Dfa(table, start, acc) as d:
+        got = d.match(to_dev(torch, x, offset), opts)
+    if ref.status == oracle.ESYMBOL:
+        assert got.status == parem.PAREM_ESYMBOL and got.bad_offset == ref.bad_offset, (got, ref)
+        return got
+    assert got.status == 0, got
+    assert (got.final_state, got.accepted, got.match_count) == (ref.final_state, ref.accepted, ref.match_count), \
+        (got, ref, table.shape, x.size, opts and (opts.chunk_len, opts.boundary_policy, opts.candidates, opts.kernel))
+    return got
+
+
+# ---------------------------------------------------------------- configs, CI-sized
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("n", [1 << 20, (1 << 20) + 13])
+def test_configs_small(parem, torch_mod, k, n):
+    c = synth.config(k, n=n)
+    x = c.make_input()
+    check(parem, torch_mod, c.table, c.start, c.accept, x)
+
+
+# ---------------------------------------------------------------- random DFAs
+def rand_dfa(rng, Q, A, partial):
+    seed = int(rng.integers(0, 1 << 30))
+    dt = np.uint16 if rng.random() < 0.6 else np.uint32
+    t = synth.partial_dfa(Q, A, float(rng.choice([0.02, 0.1, 0.4])), seed, dt) if partial else \
+        synth.random_dfa(Q, A, seed, dt)
+    acc = rng.random(Q) < float(rng.choice([0.05, 0.3, 0.9]))
+    return t, int(rng.integers(0, Q)), acc
+
+
+SIZES = [0, 1, 2, 15, 16, 17, 255, 1000, 4097, 65539]
+
+
+@pytest.mark.parametrize("seed", range(120))
+def test_random_dfas(parem, torch_mod, seed):
+    rng = np.random.default_rng(seed)
+    Q = int(rng.choice([1, 2, 3, 5, 13, 31, 32, 33, 100, 256, 1024]))
+    A = int(rng.choice([1, 2, 3, 4, 5, 26, 256]))
+    t, q0, acc = rand_dfa(rng, Q, A, partial=seed % 4 == 0)
+    for n in rng.choice(SIZES, 3, replace=False):
+        n = int(n)
+        x = rng.integers(0, A, n).astype(np.uint8)
+        opts = parem.options(chunk_len=int(rng.choice([0, 1, 3, 16, 100, 4096])),
+                             boundary=str(rng.choice(["grid", "snap"])),
+                             candidates=str(rng.choice(["parem", "parem", "enum"])))
+        check(parem, torch_mod, t, q0, acc, x, opts, offset=int(rng.integers(0, 16)))
+
+
+@pytest.mark.parametrize("kernel", ["tiny", "lanes"])
+@pytest.mark.parametrize("seed", range(30))
+def test_both_kernels_agree(parem, torch_mod, kernel, seed):
+    """The lanes kernel also handles small DFAs when forced (DFAs <= 32 states have a lanes
+    table only when > 32 states, so the tiny case forces only where allowed)."""
+    rng = np.random.default_rng(5000 + seed)
+    Q = int(rng.choice([2, 7, 13, 30])) if kernel == "tiny" else int(rng.choice([40, 300, 2000]))
+    A = int(rng.choice([2, 4, 26, 256]))
+    t, q0, acc = rand_dfa(rng, Q, A, partial=seed % 3 == 0)
+    n = int(rng.integers(1, 200000))
+    x = rng.integers(0, A, n).astype(np.uint8)
+    check(parem, torch_mod, t, q0, acc, x, parem.options(kernel=kernel), offset=seed % 16)
+
+
+@pytest.mark.parametrize("L", [1, 2, 3, 7, 16, 17, 64, 1000])
+def test_forced_chunk_lengths_kmp(parem, torch_mod, L):
+    """Chunking invariance on the DNA-motif DFA: any chunk length composes to the
+    sequential result, with both boundary policies."""
+    P = synth.cfg2_pattern()
+    t = synth.kmp_dfa(P, 4, np.uint16)
+    acc = np.zeros(13, dtype=bool)
+    acc[12] = True
+    rng = np.random.default_rng(L)
+    x = rng.integers(0, 4, 20000).astype(np.uint8)
+    for pos in rng.integers(0, 20000 - 12, 50):
+        x[pos:pos + 12] = P
+    for b in ("grid", "snap"):
+        got = check(parem, torch_mod, t, 0, acc, x, parem.options(chunk_len=L, boundary=b))
+        assert got.match_count >= 40
+
+
+# ---------------------------------------------------------------- stats vs the paper's rule
+@pytest.mark.parametrize("k,L", [(1, 64), (2, 256), (2, 1000), (3, 4096), (5, 8192)])
+def test_route_stats_grid(parem, torch_mod, k, L):
+    """routes = sum_i |R_i| and route_steps = sum_i |R_i| len_i for the grid partition,
+    computed by the oracle directly from R_i = S(T[b_i]) n L(T[b_i - 1])."""
+    c = synth.config(k, n=300000)
+    x = c.make_input()
+    with parem.Dfa(c.table, c.start, c.accept) as d:
+        got = d.match(to_dev(torch_mod, x), parem.options(chunk_len=L, boundary="grid"))
+    b = oracle.grid_boundaries(x.size, L)
+    assert got.num_chunks == len(b) - 1
+    assert (got.routes, got.route_steps) == oracle.route_stats(c.table, x, b)
+
+
+def test_route_stats_partial_and_enum(parem, torch_mod):
+    rng = np.random.default_rng(77)
+    t = synth.partial_dfa(20, 4, 0.3, 77, np.uint16)
+    acc = rng.random(20) < 0.3
+    x = rng.integers(0, 4, 50000).astype(np.uint8)
+    with parem.Dfa(t, 3, acc) as d:
+        xd = to_dev(torch_mod, x)
+        got = d.match(xd, parem.options(chunk_len=97, boundary="grid"))
+        b = oracle.grid_boundaries(x.size, 97)
+        assert (got.routes, got.route_steps) == oracle.route_stats(t, x, b)
+        en = d.match(xd, parem.options(chunk_len=97, boundary="grid", candidates="enum"))
+        p = len(b) - 1
+        assert en.routes == 1 + (p - 1) * 20            # (p-1)|Q| + 1
+        assert (en.final_state, en.match_count) == (got.final_state, got.match_count)
+
+
+def test_snap_reduces_work(parem, torch_mod):
+    c = synth.config(2, n=1 << 22)
+    x = c.make_input()
+    with parem.Dfa(c.table, 0, c.accept) as d:
+        xd = to_dev(torch_mod, x)
+        g = d.match(xd, parem.options(chunk_len=4096, boundary="grid"))
+        s = d.match(xd, parem.options(chunk_len=4096, boundary="snap"))
+    assert g.num_chunks == s.num_chunks
+    W_grid, W_exec = g.route_steps / x.size, s.route_steps / x.size
+    assert abs(W_grid - 3.75) < 0.05          # 15/4 for any 12-mer (closed form)
+    assert W_exec < 2.05                      # min_c |L(c)| = 2 for the seed-2 pattern
+    assert (g.final_state, g.match_count) == (s.final_state, s.match_count)
+
+
+# ---------------------------------------------------------------- edge cases
+def test_empty_input(parem, torch_mod):
+    for acc0 in (False, True):
+        acc = np.array([acc0, False])
+        t = np.array([[1, 0], [0, 1]], dtype=np.uint16)
+        check(parem, torch_mod, t, 0, acc, np.zeros(0, np.uint8))
+
+
+@pytest.mark.parametrize("Q,A", [(4, 2), (13, 4), (9, 5), (256, 26), (1024, 256)])
+def test_symbol_errors_smallest_offset(parem, torch_mod, Q, A):
+    rng = np.random.default_rng(Q * A)
+    t = synth.random_dfa(Q, A, 3, np.uint16)
+    acc = rng.random(Q) < 0.2
+    if A == 256:
+        pytest.skip("every byte is a valid symbol")
+    for trial in range(4):
+        x = rng.integers(0, A, 100000).astype(np.uint8)
+        bad = np.sort(rng.integers(0, x.size, 3))
+        x[bad] = rng.integers(A, 256, 3)
+        got = check(parem, torch_mod, t, 0, acc, x, parem.options(chunk_len=int(rng.choice([0, 5, 300]))))
+        assert got.status == parem.PAREM_ESYMBOL and got.bad_offset == bad[0]
+
+
+def test_dead_semantics_counterexample(parem, torch_mod):
+    """C9: delta(1,a) = DEAD; "aa" must die at the chunk boundary even when R_1 = {} ."""
+    t = np.array([[1, 0], [0xFFFF, 0]], dtype=np.uint16)
+    acc = np.array([False, True])
+    for x in ([0, 0], [0, 0, 1, 1, 0], [1, 0, 1, 0, 0, 1]):
+        for L in (1, 2, 3):
+            check(parem, torch_mod, t, 0, acc, np.array(x, np.uint8), parem.options(chunk_len=L))
+
+
+def test_worked_example_table2(parem, torch_mod):
+    """The paper's worked example (Table II): count 1, final 0, 4 chunks of 6."""
+    t = synth.kmp_dfa([0, 1, 2, 1, 4, 4, 3, 4], 5, np.uint32)
+    acc = np.zeros(9, dtype=bool)
+    acc[8] = True
+    x = np.array(["parel".index(ch) for ch in "plaraparallelapareparapl"], np.uint8)
+    got = check(parem, torch_mod, t, 0, acc, x, parem.options(chunk_len=6, boundary="grid"))
+    assert (got.final_state, got.match_count, got.num_chunks, got.routes) == (0, 1, 4, 6)
+    en = check(parem, torch_mod, t, 0, acc, x, parem.options(chunk_len=6, boundary="grid", candidates="enum"))
+    assert en.routes == 28
+
+
+# ---------------------------------------------------------------- async / continue / host
+def test_async_continue_and_host(parem, torch_mod):
+    torch = torch_mod
+    c = synth.config(3, n=3_000_017)
+    x = c.make_input()
+    ref = oracle.walk(c.table, c.start, c.accept, x)
+    with parem.Dfa(c.table, c.start, c.accept) as d:
+        xd = to_dev(torch, x)
+        ws = torch.empty(d.workspace_bytes(x.size), dtype=torch.uint8, device="cuda")
+        res = torch.zeros(64, dtype=torch.uint8, device="cuda")
+        d.match_async(xd, ws, res)
+        got = parem.MatchResult.from_bytes(res.cpu().numpy().tobytes()[:56])
+        assert (got.final_state, got.accepted, got.match_count) == (ref.final_state, ref.accepted, ref.match_count)
+        # streaming: three segments with carried state
+        cuts = [0, 1_000_003, 2_000_000, x.size]
+        ws2 = torch.empty(d.workspace_bytes(x.size), dtype=torch.uint8, device="cuda")
+        for i in range(3):
+            seg = xd[cuts[i]:cuts[i + 1]]
+            d.match_continue_async(seg, cuts[i], ws2, res if i else None, res)
+        got = parem.MatchResult.from_bytes(res.cpu().numpy().tobytes()[:56])
+        assert (got.final_state, got.accepted, got.match_count) == (ref.final_state, ref.accepted, ref.match_count)
+        h = torch.from_numpy(x).pin_memory()
+        got = d.match_host(h)
+        assert (got.final_state, got.accepted, got.match_count) == (ref.final_state, ref.accepted, ref.match_count)
+
+
+def test_host_path_symbol_error_offset(parem, torch_mod):
+    c = synth.config(2, n=(64 << 20) + 1000)
+    x = c.make_input()
+    x[(64 << 20) + 17] = 9        # in the second 64 MiB segment
+    with parem.Dfa(c.table, 0, c.accept) as d:
+        got = d.match_host(x)
+    assert got.status == parem.PAREM_ESYMBOL and got.bad_offset == (64 << 20) + 17
+
+
+# ---------------------------------------------------------------- full BASELINE sizes
+@pytest.mark.slow
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_configs_full_size(parem, torch_mod, k):
+    """BASELINE.json configs at full size, default (bench) launch configuration,
+    bit-exact against the single-threaded oracle."""
+    c = synth.config(k)
+    x = c.make_input()
+    ref = oracle.walk(c.table, c.start, c.accept, x)
+    with parem.Dfa(c.table, c.start, c.accept) as d:
+        xd = torch_mod.from_numpy(x).to("cuda")
+        got = d.match(xd)
+    assert got.status == 0
+    assert (got.final_state, got.accepted, got.match_count) == (ref.final_state, ref.accepted, ref.match_count)
