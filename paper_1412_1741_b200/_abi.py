@@ -5,7 +5,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libparem.so")
+SO_PATH = os.environ.get("PAREM_LIB") or os.path.join(_HERE, "libparem.so")
 
 PAREM_OK, PAREM_EINVAL, PAREM_ESYMBOL, PAREM_ECUDA, PAREM_ENOMEM, PAREM_EINTERNAL = 0, -1, -2, -3, -4, -5
 PAREM_DEAD = 0xFFFFFFFF

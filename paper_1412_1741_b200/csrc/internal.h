@@ -24,7 +24,7 @@
 namespace parem {
 
 constexpr uint32_t kTinyMaxStates = 32;   // dense per-chunk maps live in one warp
-constexpr uint32_t kTinyThreads = 256;    // threads (= chunks) per CTA, tiny kernel
+constexpr uint32_t kTinyThreads = 512;    // threads (= chunks) per CTA, tiny kernel
 constexpr uint32_t kTinyMaxA = 256;
 constexpr uint32_t kKernelTrivial = 0, kKernelTiny = 1, kKernelLanes = 2;
 
@@ -77,6 +77,7 @@ struct Plan {
     uint32_t sym_per_lookup;
     uint32_t win;
     uint32_t smem_tab;       // lanes: table staged in shared memory
+    uint32_t tma;            // tiny: rows staged by TMA when the input is 16-B aligned
     size_t smem;
     size_t ws;
     size_t off_maps, off_hits;
@@ -104,8 +105,8 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
 int launch_tiny(const Plan& plan, const MatchParams& P, cudaStream_t s);
 int launch_lanes(const Plan& plan, const MatchParams& P, cudaStream_t s);
 int launch_trivial(const MatchParams& P, cudaStream_t s);
-int tiny_blocks_per_sm(uint32_t K, uint32_t B, size_t smem);
-size_t tiny_smem_bytes(const DevDfa& d, uint32_t B);
+int tiny_blocks_per_sm(uint32_t K, uint32_t B, bool tma, size_t smem);
+size_t tiny_smem_bytes(const DevDfa& d, uint32_t B, bool tma);
 size_t lanes_smem_bytes(const DevDfa& d, bool smem_tab);
 int lanes_blocks_per_sm(uint32_t U, bool smem_tab, bool u32, uint32_t threads, size_t smem);
 uint32_t tiny_round_slots(uint32_t k);

@@ -30,7 +30,7 @@ static int cached_bps(int kind, uint32_t a, uint32_t b, uint32_t c, uint32_t thr
         auto it = cache.find(key);
         if (it != cache.end()) return it->second;
     }
-    int v = kind == 1 ? tiny_blocks_per_sm(a, b, smem) : lanes_blocks_per_sm(a, b != 0, c != 0, threads, smem);
+    int v = kind == 1 ? tiny_blocks_per_sm(a, b, c != 0, smem) : lanes_blocks_per_sm(a, b != 0, c != 0, threads, smem);
     std::lock_guard<std::mutex> g(mu);
     cache[key] = v;
     return v;
@@ -76,17 +76,19 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         uint32_t need = cand == PAREM_CANDIDATES_ENUM ? d.Q : (policy == PAREM_BOUNDARY_SNAP ? d.Lmin : d.Lmax);
         if (need < 1) need = 1;
         const uint32_t K = tiny_round_slots(need);
-        const size_t smem = tiny_smem_bytes(d, B);
-        int bps = cached_bps(1, K, B, 0, kTinyThreads, smem);
+        const bool tma = forced == 0 || forced % 64 == 0;
+        const size_t smem = tiny_smem_bytes(d, B, tma);
+        int bps = cached_bps(1, K, B, tma, kTinyThreads, smem);
         if (bps <= 0) { set_error("tiny kernel does not fit (smem %zu)", smem); return PAREM_EINVAL; }
         uint64_t L;
         if (forced) L = forced;
         else {
             const uint64_t target = (uint64_t)sms * bps * kTinyThreads;
             L = ceil_div(n, target);
-            L = (L + 15) & ~15ull;
+            L = (L + 63) & ~63ull;       // whole TMA boxes per row
             if (L < 256) L = 256;
         }
+        plan->tma = tma;
         if (L > (1ull << 30)) L = 1ull << 30;
         const uint64_t p = n / L ? n / L : 1;
         plan->threads = kTinyThreads;

@@ -252,3 +252,33 @@ def test_configs_full_size(parem, torch_mod, k):
         got = d.match(xd)
     assert got.status == 0
     assert (got.final_state, got.accepted, got.match_count) == (ref.final_state, ref.accepted, ref.match_count)
+
+
+# ---------------------------------------------------------------- route merging stress
+@pytest.mark.parametrize("Q", [3, 5, 13, 31])
+def test_permutation_dfa_routes_never_merge(parem, torch_mod, Q):
+    """delta(q, c) = (q + c + 1) mod Q: every column is a permutation (|L(c)| = Q, the
+    paper's worst case P:70), so a chunk's routes never converge."""
+    A = 4
+    t = np.array([[(q + c + 1) % Q for c in range(A)] for q in range(Q)], dtype=np.uint16)
+    acc = np.zeros(Q, dtype=bool)
+    acc[Q // 2] = True
+    x = synth.uniform_symbols((1 << 20) + 33, A, seed=Q)
+    for b in ("snap", "grid"):
+        check(parem, torch_mod, t, 1, acc, x, parem.options(boundary=b))
+
+
+@pytest.mark.parametrize("p_reset", [1e-4, 1e-3, 2e-2])
+def test_partially_merging_warps(parem, torch_mod, p_reset):
+    """A mod-Q counter with a rare reset symbol: chunks that contain a reset merge their
+    routes, the others do not -- lanes of one warp disagree."""
+    Q, A = 11, 4
+    t = np.array([[(q + 1) % Q if c < 3 else 0 for c in range(A)] for q in range(Q)], dtype=np.uint16)
+    acc = np.zeros(Q, dtype=bool)
+    acc[[0, 7]] = True
+    rng = np.random.default_rng(int(1 / p_reset))
+    x = rng.integers(0, 3, 4 << 20).astype(np.uint8)
+    x[rng.random(x.size) < p_reset] = 3
+    for b in ("grid", "snap"):
+        for L in (0, 4096, 8192 + 64):
+            check(parem, torch_mod, t, 0, acc, x, parem.options(boundary=b, chunk_len=L))
