@@ -161,7 +161,9 @@ extern "C" int parem_dfa_create(uint32_t Q, uint32_t A, const void* table, uint3
                 }
         }
     } else {
-        lanes_u32 = Qpad > 16384;
+        // u32 entries when the table is staged in shared memory (32-bit LDS takes the
+        // [reg + uniform base] form) or when dest*2 no longer fits 15 bits
+        lanes_u32 = Qpad > 16384 || (size_t)Apad * Qpad * 4 <= (size_t)160 * 1024;
         const uint32_t ES = lanes_u32 ? 4 : 2;
         lanes.assign((size_t)Apad * Qpad * ES, 0);
         for (uint32_t c = 0; c < A; ++c)

@@ -60,6 +60,7 @@ struct MatchParams {
     uint64_t L;                // nominal chunk length
     uint64_t p;                // number of chunks
     uint32_t policy, cand, win, slots;
+    uint32_t tg, pad_tg;       // lanes: threads per chunk group
     uint64_t offset_base;
     const parem_result* carry; // may be null
     parem_result* result;
@@ -74,6 +75,7 @@ struct Plan {
     uint64_t grid;
     uint64_t p, L;
     uint32_t policy, cand, slots, U;
+    uint32_t tg;             // lanes: threads per chunk group (blockDim = G * tg)
     uint32_t sym_per_lookup;
     uint32_t win;
     uint32_t smem_tab;       // lanes: table staged in shared memory
@@ -110,5 +112,5 @@ size_t tiny_smem_bytes(const DevDfa& d, uint32_t B, bool tma);
 size_t lanes_smem_bytes(const DevDfa& d, bool smem_tab);
 int lanes_blocks_per_sm(uint32_t U, bool smem_tab, bool u32, uint32_t threads, size_t smem);
 uint32_t tiny_round_slots(uint32_t k);
-uint32_t lanes_round_u(uint32_t u);
+uint32_t lanes_max_groups();
 }  // namespace parem

@@ -112,16 +112,29 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
     const bool smem_tab = tab_bytes <= (size_t)160 * 1024;
     uint32_t S = cand == PAREM_CANDIDATES_ENUM ? d.Q : d.Lmax;
     if (S < 1) S = 1;
-    uint32_t U = S <= 64 ? 1 : S <= 2048 ? 2 : S <= 4096 ? 4 : 8;
-    uint64_t T = 32 * ceil_div(S, 32ull * U);
-    if (T > 1024) T = 1024;
+    // choose U (routes per thread) and Tg (threads per chunk) minimising the issue cost of
+    // one byte: Tg * (3 U + 3) (3 instructions per route-step + ~3 shared per byte)
+    static const uint32_t Us[] = {1, 2, 3, 4, 6, 8};
+    uint32_t U = 1;
+    uint64_t Tg = 32, best = ~0ull;
+    for (uint32_t u : Us) {
+        uint64_t tg = 32 * ceil_div(S, 32ull * u);
+        if (tg > 1024) continue;
+        const uint64_t cost = tg * (3ull * u + 3);
+        if (cost < best) { best = cost; U = u; Tg = tg; }
+    }
+    if (best == ~0ull) { U = 8; Tg = 1024; }           // > 8192 candidates: extra passes
+    // several chunks per CTA share the staged table: up to 512 threads per CTA
+    uint64_t G = Tg >= 512 ? 1 : 512 / Tg;
+    if (G > lanes_max_groups()) G = lanes_max_groups();
+    const uint64_t T = G * Tg;
     const size_t smem = lanes_smem_bytes(d, smem_tab);
     int bps = cached_bps(2, U, smem_tab, d.lanes_u32, (uint32_t)T, smem);
     if (bps <= 0) { set_error("lanes kernel does not fit (smem %zu, threads %llu)", smem, (unsigned long long)T); return PAREM_EINVAL; }
     uint64_t L;
     if (forced) L = forced;
     else {
-        const uint64_t target = (uint64_t)sms * bps;
+        const uint64_t target = (uint64_t)sms * bps * G;   // one wave of chunk groups
         L = ceil_div(n, target);
         L = (L + 15) & ~15ull;
         if (L < 4096) L = 4096;
@@ -129,10 +142,11 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
     if (L > (1ull << 30)) L = 1ull << 30;
     const uint64_t p = n / L ? n / L : 1;
     plan->threads = (uint32_t)T;
-    plan->grid = p;
+    plan->tg = (uint32_t)Tg;
+    plan->grid = ceil_div(p, G);
     plan->p = p;
     plan->L = L;
-    plan->slots = (uint32_t)(T * U);
+    plan->slots = (uint32_t)(Tg * U);
     plan->U = U;
     plan->sym_per_lookup = 1;
     plan->win = (policy == PAREM_BOUNDARY_SNAP && L > 1) ? (uint32_t)(L - 1 < 4096 ? L - 1 : 4096) : 0;
