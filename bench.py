@@ -105,6 +105,31 @@ def dist_env():
     return ws, rank, local
 
 
+def rank_input(cfg, rank: int, n: int | None = None):
+    """Rank-distinct input of the configured workload (weak scaling): rank 0 gets the
+    config's own input; rank r > 0 continues the counter-based stream at offset r*n
+    (uniform configs) or uses seed + 1000 r (Markov config)."""
+    import synth
+
+    n = cfg.n if n is None else n
+    if rank == 0:
+        return cfg.make_input(n)
+    if cfg.input_kind == "markov":
+        return synth.markov_bytes(n, cfg.input_seed + 1000 * rank)
+    return synth.uniform_symbols(n, cfg.A, cfg.input_seed, 0, rank * n)
+
+
+def reduce_max(value: float, dist, device) -> float:
+    """Max over ranks (device time of the slowest rank) -- identity when not distributed."""
+    if dist is None:
+        return value
+    import torch
+
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def cpu_baseline(cfg, x, budget_s: float = 12.0, max_bytes: int = 256 << 20):
     """The oracle as it stands: single-threaded C walk, on a bounded sample of the input."""
     import oracle
@@ -158,10 +183,15 @@ def run_reference(args):
 
 def latest_traffic(cfg_index: int):
     """dram bytes per launch from the committed ncu --set full summary, if any."""
-    p = os.path.join(ROOT, "profiles", f"ncu_full_cfg{cfg_index}.json")
+    import glob
+
+    cands = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_full_cfg{cfg_index}.json")))
+    if not cands:
+        return None
     try:
-        with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+        with open(cands[-1]) as f:
+            v = json.load(f).get("dram_bytes_per_launch")
+        return {"dram_bytes_per_launch": v, "source": os.path.relpath(cands[-1], ROOT)} if v else None
     except Exception:
         return None
 
@@ -179,6 +209,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-micro", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=64 << 20)
     ap.add_argument("--verify", action="store_true", help="bit-exact check against the oracle (full size)")
     args = ap.parse_args()
@@ -205,12 +236,9 @@ def main():
 
     cfg = synth.config(args.config)
     n = cfg.n
-    # rank-distinct input (weak scaling): offset the counter-based stream by rank * n
-    if cfg.input_kind == "markov":
-        x = synth.markov_bytes(n, cfg.input_seed + 1000 * rank) if rank else cfg.make_input()
-    else:
-        x = synth.uniform_symbols(n, cfg.A, cfg.input_seed, 0, rank * n)
-    xd = torch.from_numpy(x).to(f"cuda:{local}")
+    x = rank_input(cfg, rank)
+    dev = torch.device("cuda", local)
+    xd = torch.from_numpy(x).to(dev)
     dfa = P.Dfa(cfg.table, cfg.start, cfg.accept)
     opts = P.options(chunk_len=args.chunk_len, boundary=args.boundary, candidates=args.candidates)
     plan = dfa.plan(n, opts)
@@ -238,12 +266,8 @@ def main():
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    t_ms = ev0.elapsed_time(ev1)
+    t_ms = reduce_max(ev0.elapsed_time(ev1), dist, dev)
     launch_ms = [a.elapsed_time(b) for a, b in per]
-    if dist:
-        tt = torch.tensor([t_ms], device=f"cuda:{local}")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
     r = P.MatchResult.from_bytes(res.cpu().numpy().tobytes()[:56])
     assert r.status == 0, r
 
@@ -261,11 +285,7 @@ def main():
         t0 = time.perf_counter()
         for _ in range(e_steps):
             rh = dfa.match_host(hx)
-        t_e2e = (time.perf_counter() - t0) / e_steps
-        if dist:
-            tt = torch.tensor([t_e2e], device=f"cuda:{local}")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            t_e2e = float(tt.item())
+        t_e2e = reduce_max((time.perf_counter() - t0) / e_steps, dist, dev)
         assert (rh.final_state, rh.match_count) == (r.final_state, r.match_count)
         e2e = {"value": round(n * ws_ / t_e2e / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": int(n),
                "d2h_bytes_per_step": 56, "ms_per_step": round(1e3 * t_e2e, 3), "api": "parem_match_host"}
@@ -282,7 +302,7 @@ def main():
                                        C.c_void_p(stream.cuda_stream))
         micro["read_stream_gbs"] = round(n / (ms * 1e-3) / 1e9, 1) if ms > 0 else None
         rng = np.random.default_rng(0)
-        for where, nm, ent in ((2, "smem_lane_private", 1 << 10), (0, "smem_random_16KiB", 1 << 13),
+        for where, nm, ent in ((2, "smem_lane_private_32KiB", 1 << 8), (0, "smem_random_32KiB", 1 << 13),
                                (1, "l2_random_2MiB", 1 << 20)):
             tabx = torch.from_numpy(rng.integers(0, 1 << 16, ent).astype(np.uint16)).to(xd.device)
             lk = C.c_uint64()
@@ -290,6 +310,37 @@ def main():
                                       C.byref(lk), 3, C.c_void_p(stream.cuda_stream))
             micro[f"gather_{nm}_lookups_per_s"] = float(f"{lk.value / (ms * 1e-3):.4g}") if ms > 0 else None
         torch.cuda.synchronize()
+
+    # ---- small inputs (cfg1): steady-state throughput of a CUDA graph of K back-to-back
+    # matches over K distinct buffers (K * n >= 2x L2, so it is HBM-honest; SURVEY §8(d) note 1)
+    graph_batched = None
+    if n <= (16 << 20) and not args.no_graph:
+        K = max(8, (256 << 20) // n)
+        bufs = torch.empty((K, n), dtype=torch.uint8, device=dev)
+        for i in range(K):
+            bufs[i].copy_(torch.from_numpy(rank_input(cfg, rank * K + i)))
+        gs = torch.cuda.Stream(device=dev)
+        gs.wait_stream(stream)
+        with torch.cuda.stream(gs):
+            dfa.match_async(bufs[0], wsb, res, opts, gs)   # warm (plan cache, attributes)
+            gs.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=gs):
+                for i in range(K):
+                    dfa.match_async(bufs[i], wsb, res, opts, gs)
+            graph.replay()
+            gs.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(gs)
+            for _ in range(3):
+                graph.replay()
+            g1.record(gs)
+            gs.synchronize()
+        gms = reduce_max(g0.elapsed_time(g1) / 3, dist, dev)
+        rg = P.MatchResult.from_bytes(res.cpu().numpy().tobytes()[:56])
+        graph_batched = {"value": round(K * n * ws_ / (gms * 1e-3) / 1e9, 2), "unit": UNIT, "buffers": K,
+                         "bytes_per_buffer": n, "ms_per_graph": round(gms, 4),
+                         "us_per_match": round(1e3 * gms / K, 3), "last_count": rg.match_count}
 
     clocks = clk.summary()
     sm_clk = clocks["sm_mhz"] or sm_mhz_max
@@ -330,6 +381,7 @@ def main():
         "clocks": clocks,
         "e2e": e2e,
         "micro": micro,
+        "graph_batched": graph_batched,
     }
     if not args.no_cpu_baseline and rank == 0 and ws_ == 1:
         line["cpu_baseline"] = cpu_baseline(cfg, x)

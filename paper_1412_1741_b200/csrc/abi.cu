@@ -224,37 +224,41 @@ __global__ void __launch_bounds__(512) read_stream_kernel(const uint4* __restric
     if (acc == 0x9E3779B9u) sink[0] = acc;   // practically never; keeps the loads alive
 }
 
-// Dependent random u16 gathers: 4 independent chains per thread, `steps` steps each.
-// where = 0: table in shared memory (random banks); 1: global / L2; 2: shared memory,
-// lane-private (word w of lane l at w*32 + l: conflict-free by construction).
+// Dependent random gathers, 8 independent chains per thread, `steps` steps each, so the
+// LSU (not the chain latency) is the limit at full occupancy.
+// where = 0: u32 table in shared memory (random banks, the lanes kernel's access pattern);
+//         1: u16 table in global memory / L2;
+//         2: u32 table in shared memory, lane-private (word w of lane l at w*32 + l:
+//            conflict-free by construction -- the tiny kernel's stride-table pattern).
 template <int WHERE>
 __global__ void __launch_bounds__(256) gather_kernel(const uint16_t* __restrict__ tab, uint32_t entries,
                                                      uint32_t steps, uint32_t* sink) {
     extern __shared__ __align__(16) unsigned char smb[];
     const uint32_t tid = threadIdx.x, lane = tid & 31u;
     const uint32_t mask = entries - 1u;   // entries is a power of two
+    uint32_t* t32 = reinterpret_cast<uint32_t*>(smb);
     if (WHERE == 0)
-        for (uint32_t i = tid; i < entries; i += blockDim.x) reinterpret_cast<uint16_t*>(smb)[i] = tab[i];
+        for (uint32_t i = tid; i < entries; i += blockDim.x) t32[i] = tab[i];
     if (WHERE == 2)
-        for (uint32_t i = tid; i < entries * 32u; i += blockDim.x)
-            reinterpret_cast<uint32_t*>(smb)[i] = tab[i >> 5];
+        for (uint32_t i = tid; i < entries * 32u; i += blockDim.x) t32[i] = tab[i >> 5];
     __syncthreads();
-    uint32_t x0 = (blockIdx.x * 977u + tid * 131u) & mask, x1 = (x0 + 1) & mask, x2 = (x0 + 7) & mask,
-             x3 = (x0 + 13) & mask;
+    uint32_t x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = (blockIdx.x * 977u + tid * 131u + 37u * k) & mask;
     for (uint32_t s = 0; s < steps; ++s) {
-        if (WHERE == 0) {
-            const uint16_t* t = reinterpret_cast<const uint16_t*>(smb);
-            x0 = (t[x0] + s) & mask; x1 = (t[x1] + s) & mask; x2 = (t[x2] + s) & mask; x3 = (t[x3] + s) & mask;
-        } else if (WHERE == 1) {
-            x0 = (__ldg(tab + x0) + s) & mask; x1 = (__ldg(tab + x1) + s) & mask;
-            x2 = (__ldg(tab + x2) + s) & mask; x3 = (__ldg(tab + x3) + s) & mask;
-        } else {
-            const uint32_t* t = reinterpret_cast<const uint32_t*>(smb);
-            x0 = (t[x0 * 32u + lane] + s) & mask; x1 = (t[x1 * 32u + lane] + s) & mask;
-            x2 = (t[x2 * 32u + lane] + s) & mask; x3 = (t[x3 * 32u + lane] + s) & mask;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            uint32_t v;
+            if (WHERE == 0) v = t32[x[k]];
+            else if (WHERE == 1) v = __ldg(tab + x[k]);
+            else v = t32[x[k] * 32u + lane];
+            x[k] = (v + s) & mask;
         }
     }
-    if ((x0 ^ x1 ^ x2 ^ x3) == 0xFFFFFFFFu) sink[0] = x0;
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc ^= x[k];
+    if (acc == 0xFFFFFFFFu) sink[0] = acc;
 }
 
 }  // namespace parem
@@ -291,7 +295,7 @@ extern "C" float parem_bench_gather(uint32_t where, const uint16_t* d_table, uin
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    size_t smem = where == 0 ? entries * 2 : where == 2 ? (size_t)entries * 128 : 0;
+    size_t smem = where == 0 ? (size_t)entries * 4 : where == 2 ? (size_t)entries * 128 : 0;
     if (smem > 200 * 1024) return (float)PAREM_EINVAL;
     const void* fn = where == 0 ? (const void*)gather_kernel<0> : where == 1 ? (const void*)gather_kernel<1>
                                                                            : (const void*)gather_kernel<2>;
@@ -313,7 +317,7 @@ extern "C" float parem_bench_gather(uint32_t where, const uint16_t* d_table, uin
     cudaEventElapsedTime(&ms, a, b);
     cudaEventDestroy(a);
     cudaEventDestroy(b);
-    if (lookups_out) *lookups_out = (uint64_t)grid * 256 * 4 * steps;
+    if (lookups_out) *lookups_out = (uint64_t)grid * 256 * 8 * steps;
     if (cudaGetLastError() != cudaSuccess) return (float)PAREM_ECUDA;
     return ms / reps;
 }
