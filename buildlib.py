@@ -6,6 +6,7 @@ All artefacts are built in-tree so they travel to the GPU box with the gpurun sn
 """
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
 import subprocess
@@ -66,14 +67,27 @@ def build_parem(force: bool = False, verbose_ptxas: bool = False) -> str:
         return PAREM_SO
     objdir = os.path.join(ROOT, "build", "obj")
     os.makedirs(objdir, exist_ok=True)
+    d = os.path.join(ROOT, "paper_1412_1741_b200", "csrc")
+    headers = sorted(glob.glob(os.path.join(d, "*.cuh")) + glob.glob(os.path.join(d, "*.h"))) + [
+        os.path.join(ROOT, "include", "parem.h")
+    ]
+    jobs = []
     objs = []
     for src in parem_sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        if not (force or _stale(obj, [src] + headers)):
+            continue
         flags = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-lineinfo"]
         if src.endswith(".cu"):
             flags += ARCH + ["-Xptxas", "-v"] if verbose_ptxas else ARCH
-        _run([NVCC, "-c", src, "-o", obj] + flags)
-        objs.append(obj)
+        jobs.append([NVCC, "-c", src, "-o", obj] + flags)
+    # the tiny-kernel instantiation TUs dominate: compile every object in parallel
+    workers = max(1, min(len(jobs), os.cpu_count() or 1))
+    if jobs:
+        with concurrent.futures.ThreadPoolExecutor(workers) as ex:
+            for f in [ex.submit(_run, j) for j in jobs]:
+                f.result()
     _run([NVCC, "-shared", "-o", PAREM_SO] + objs + ARCH)
     return PAREM_SO
 
