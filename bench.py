@@ -203,7 +203,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--boundary", default="snap", choices=["snap", "grid"])
+    ap.add_argument("--boundary", default="auto", choices=["auto", "snap", "grid"])
     ap.add_argument("--candidates", default="parem", choices=["parem", "enum"])
     ap.add_argument("--chunk-len", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -368,7 +368,8 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (seeded, SURVEY §8(d) recipe; no public dataset in the paper)",
         "config": {"workload": f"cfg{cfg.index}: {cfg.name}", "n_bytes": n, "states": cfg.Q, "alphabet": cfg.A,
-                   "boundary": args.boundary, "candidates": args.candidates, "kernel": plan["kernel"],
+                   "boundary": {0: "grid", 1: "snap"}.get(plan["boundary_policy"], args.boundary),
+                   "candidates": args.candidates, "kernel": plan["kernel"],
                    "chunks": plan["num_chunks"], "chunk_len": plan["chunk_len"], "grid": plan["grid_blocks"],
                    "block": plan["block_threads"], "slots": plan["slots"],
                    "l2": "input larger than L2 (no flush needed)" if n > (126 << 20) else "input fits L2 (warm)",

@@ -52,6 +52,8 @@ extern "C" {
 /* boundary_policy */
 #define PAREM_BOUNDARY_GRID 0u   /* b_i = i * chunk_len, remainder to the last chunk (C7)   */
 #define PAREM_BOUNDARY_SNAP 1u   /* planner: move b_i forward (<= window) to minimise |L(T[b_i-1])| */
+#define PAREM_BOUNDARY_AUTO 2u   /* planner picks GRID or SNAP (GRID when every |L(c)| is small and the
+                                    thread-per-chunk kernel merges converged routes, else SNAP)   */
 /* candidates */
 #define PAREM_CANDIDATES_PAREM 0u  /* R_i = S n L (the paper's rule)                        */
 #define PAREM_CANDIDATES_ENUM 1u   /* every chunk i >= 1 starts from all of Q (Enum) */
@@ -71,7 +73,7 @@ typedef struct parem_result {
     uint32_t reserved;
 } parem_result;
 
-/* Options (NULL = defaults: planner-chosen chunk length, SNAP, PaREM candidates).
+/* Options (NULL = defaults: planner-chosen chunk length, AUTO boundaries, PaREM candidates).
  * chunk_len forces the nominal chunk length (bytes, >= 1): p = max(1, floor(n / chunk_len))
  * chunks; with GRID the remainder goes to the last chunk.  Results are independent of all
  * options (only the stats routes/route_steps/num_chunks change). */

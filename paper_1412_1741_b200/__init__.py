@@ -18,7 +18,7 @@ from typing import NamedTuple
 import numpy as np
 
 from . import _abi
-from ._abi import (BOUNDARY_GRID, BOUNDARY_SNAP, CANDIDATES_ENUM, CANDIDATES_PAREM, KERNEL_AUTO, KERNEL_LANES,
+from ._abi import (BOUNDARY_AUTO, BOUNDARY_GRID, BOUNDARY_SNAP, CANDIDATES_ENUM, CANDIDATES_PAREM, KERNEL_AUTO, KERNEL_LANES,
                    KERNEL_TINY, PAREM_DEAD, PAREM_EINVAL, PAREM_ESYMBOL, PAREM_OK)
 
 __all__ = ["Dfa", "MatchResult", "ParemError", "options", "PAREM_DEAD", "PAREM_OK", "PAREM_ESYMBOL",
@@ -55,12 +55,12 @@ class MatchResult(NamedTuple):
         return MatchResult.from_struct(_abi.parem_result.from_buffer_copy(b))
 
 
-_POLICY = {"grid": BOUNDARY_GRID, "snap": BOUNDARY_SNAP}
+_POLICY = {"grid": BOUNDARY_GRID, "snap": BOUNDARY_SNAP, "auto": BOUNDARY_AUTO}
 _CAND = {"parem": CANDIDATES_PAREM, "enum": CANDIDATES_ENUM}
 _KERNEL = {"auto": KERNEL_AUTO, "tiny": KERNEL_TINY, "lanes": KERNEL_LANES}
 
 
-def options(chunk_len: int = 0, boundary: str = "snap", candidates: str = "parem", kernel: str = "auto"):
+def options(chunk_len: int = 0, boundary: str = "auto", candidates: str = "parem", kernel: str = "auto"):
     o = _abi.parem_options()
     o.chunk_len = int(chunk_len)
     o.boundary_policy = _POLICY[boundary]

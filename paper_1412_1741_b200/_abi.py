@@ -9,7 +9,7 @@ SO_PATH = os.environ.get("PAREM_LIB") or os.path.join(_HERE, "libparem.so")
 
 PAREM_OK, PAREM_EINVAL, PAREM_ESYMBOL, PAREM_ECUDA, PAREM_ENOMEM, PAREM_EINTERNAL = 0, -1, -2, -3, -4, -5
 PAREM_DEAD = 0xFFFFFFFF
-BOUNDARY_GRID, BOUNDARY_SNAP = 0, 1
+BOUNDARY_GRID, BOUNDARY_SNAP, BOUNDARY_AUTO = 0, 1, 2
 CANDIDATES_PAREM, CANDIDATES_ENUM = 0, 1
 KERNEL_AUTO, KERNEL_TINY, KERNEL_LANES = 0, 1, 2
 

@@ -24,7 +24,8 @@
 namespace parem {
 
 constexpr uint32_t kTinyMaxStates = 32;   // dense per-chunk maps live in one warp
-constexpr uint32_t kTinyThreads = 512;    // threads (= chunks) per CTA, tiny kernel
+constexpr uint32_t kTinyThreads = 512;    // threads per CTA, tiny kernel
+constexpr uint32_t kTinyRowsPerThread = 2;  // chunks per thread, tiny kernel
 constexpr uint32_t kTinyMaxA = 256;
 constexpr uint32_t kKernelTrivial = 0, kKernelTiny = 1, kKernelLanes = 2;
 
@@ -60,7 +61,8 @@ struct MatchParams {
     uint64_t L;                // nominal chunk length
     uint64_t p;                // number of chunks
     uint32_t policy, cand, win, slots;
-    uint32_t tg, pad_tg;       // lanes: threads per chunk group
+    uint32_t tg;               // lanes: threads per chunk group
+    uint32_t stages;           // tiny: TMA stages per warp (0 = no TMA)
     uint64_t offset_base;
     const parem_result* carry; // may be null
     parem_result* result;
@@ -79,7 +81,7 @@ struct Plan {
     uint32_t sym_per_lookup;
     uint32_t win;
     uint32_t smem_tab;       // lanes: table staged in shared memory
-    uint32_t tma;            // tiny: rows staged by TMA when the input is 16-B aligned
+    uint32_t tma;            // tiny: TMA stages per warp (0 = rows read with 16-B loads)
     size_t smem;
     size_t ws;
     size_t off_maps, off_hits;
@@ -108,9 +110,10 @@ int launch_tiny(const Plan& plan, const MatchParams& P, cudaStream_t s);
 int launch_lanes(const Plan& plan, const MatchParams& P, cudaStream_t s);
 int launch_trivial(const MatchParams& P, cudaStream_t s);
 int tiny_blocks_per_sm(uint32_t K, uint32_t B, bool tma, size_t smem);
-size_t tiny_smem_bytes(const DevDfa& d, uint32_t B, bool tma);
+size_t tiny_smem_bytes(const DevDfa& d, uint32_t B, uint32_t stages);
+uint32_t tiny_pick_stages(const DevDfa& d, uint32_t B);
 size_t lanes_smem_bytes(const DevDfa& d, bool smem_tab);
 int lanes_blocks_per_sm(uint32_t U, bool smem_tab, bool u32, uint32_t threads, size_t smem);
-uint32_t tiny_round_slots(uint32_t k);
+uint32_t tiny_round_slots(uint32_t k, uint32_t B);
 uint32_t lanes_max_groups();
 }  // namespace parem

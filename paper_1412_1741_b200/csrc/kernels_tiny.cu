@@ -21,25 +21,31 @@
 
 namespace parem {
 
-const void* tiny_dispatch_b0_t0(uint32_t K);
-const void* tiny_dispatch_b0_t1(uint32_t K);
-const void* tiny_dispatch_b1_t0(uint32_t K);
-const void* tiny_dispatch_b1_t1(uint32_t K);
-const void* tiny_dispatch_b2_t0(uint32_t K);
-const void* tiny_dispatch_b2_t1(uint32_t K);
+const void* tiny_dispatch_b0_t0_0(uint32_t K);
+const void* tiny_dispatch_b0_t1_0(uint32_t K);
+const void* tiny_dispatch_b0_t1_1(uint32_t K);
+const void* tiny_dispatch_b1_t0_0(uint32_t K);
+const void* tiny_dispatch_b1_t1_0(uint32_t K);
+const void* tiny_dispatch_b1_t1_1(uint32_t K);
+const void* tiny_dispatch_b2_t0_0(uint32_t K);
+const void* tiny_dispatch_b2_t1_0(uint32_t K);
+const void* tiny_dispatch_b2_t1_1(uint32_t K);
 
 namespace {
 
 const void* tiny_dispatch(uint32_t K, uint32_t B, bool tma) {
-    switch (B * 2 + (tma ? 1 : 0)) {
-        case 0: return tiny_dispatch_b0_t0(K);
-        case 1: return tiny_dispatch_b0_t1(K);
-        case 2: return tiny_dispatch_b1_t0(K);
-        case 3: return tiny_dispatch_b1_t1(K);
-        case 4: return tiny_dispatch_b2_t0(K);
-        case 5: return tiny_dispatch_b2_t1(K);
-        default: return nullptr;
-    }
+    const void* f = nullptr;
+    const uint32_t T = tma ? 1u : 0u;
+    if (!f && B == 0 && T == 0) f = tiny_dispatch_b0_t0_0(K);
+    if (!f && B == 0 && T == 1) f = tiny_dispatch_b0_t1_0(K);
+    if (!f && B == 0 && T == 1) f = tiny_dispatch_b0_t1_1(K);
+    if (!f && B == 1 && T == 0) f = tiny_dispatch_b1_t0_0(K);
+    if (!f && B == 1 && T == 1) f = tiny_dispatch_b1_t1_0(K);
+    if (!f && B == 1 && T == 1) f = tiny_dispatch_b1_t1_1(K);
+    if (!f && B == 2 && T == 0) f = tiny_dispatch_b2_t0_0(K);
+    if (!f && B == 2 && T == 1) f = tiny_dispatch_b2_t1_0(K);
+    if (!f && B == 2 && T == 1) f = tiny_dispatch_b2_t1_1(K);
+    return f;
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
@@ -61,15 +67,40 @@ EncodeFn encode_fn() {
 
 }  // namespace
 
-uint32_t tiny_round_slots(uint32_t k) {
+// Register slots per chunk (routes advanced together).  Generic-alphabet kernels (B = 0:
+// one table lookup per symbol) are instantiated for fewer K to bound the build.
+uint32_t tiny_round_slots(uint32_t k, uint32_t B) {
     static const uint32_t ks[] = {1, 2, 3, 4, 6, 8, 12, 16};
+    static const uint32_t k0[] = {1, 2, 4, 8};
+    if (B == 0) {
+        for (uint32_t v : k0)
+            if (k <= v) return v;
+        return 8;   // more candidates: extra passes over the chunk
+    }
     for (uint32_t v : ks)
         if (k <= v) return v;
-    return 16;   // more candidates: extra passes over the chunk
+    return 16;
 }
 
-size_t tiny_smem_bytes(const DevDfa& d, uint32_t B, bool tma) {
-    return tiny_layout(d.Qp, d.Qpad, d.A, d.Lsum_all, B, tma).total;
+size_t tiny_smem_bytes(const DevDfa& d, uint32_t B, uint32_t stages) {
+    return tiny_layout(d.Qp, d.Qpad, d.A, d.Lsum_all, B, stages).total;
+}
+
+// TMA stages per warp: as many 4 KB boxes (<= kMaxStages) as fit next to the tables in one
+// CTA's opt-in shared memory; 0 = no TMA staging.  More than ~48 boxes in flight per SM
+// collapses TMA throughput (profiles/r01_stream_probe.txt), so 16 warps x 3 is the cap.
+uint32_t tiny_pick_stages(const DevDfa& d, uint32_t B) {
+    static int limit = 0;
+    if (!limit) {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || v <= 0)
+            v = 232448;
+        limit = v;
+    }
+    for (uint32_t s = kMaxStages; s >= 2; --s)
+        if (tiny_smem_bytes(d, B, s) <= (size_t)limit) return s;
+    return 0;
 }
 
 int tiny_blocks_per_sm(uint32_t K, uint32_t B, bool tma, size_t smem) {
@@ -84,7 +115,7 @@ int tiny_blocks_per_sm(uint32_t K, uint32_t B, bool tma, size_t smem) {
 int launch_tiny(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     // TMA staging needs a 16-B aligned input and rows of a multiple of the box width
     // (and every nominal row [t L, (t+1) L) inside the input: p L <= n)
-    bool tma = plan.tma && (((uintptr_t)P.in) & 15u) == 0 && P.L % kBoxBytes == 0 && P.L >= kBoxBytes &&
+    bool tma = plan.tma != 0 && (((uintptr_t)P.in) & 15u) == 0 && P.L % kBoxBytes == 0 && P.L >= kBoxBytes &&
                P.p * P.L <= P.n;
     CUtensorMap map;
     memset(&map, 0, sizeof(map));
@@ -92,7 +123,7 @@ int launch_tiny(const Plan& plan, const MatchParams& P, cudaStream_t s) {
         EncodeFn enc = encode_fn();
         const cuuint64_t dims[2] = {(cuuint64_t)P.L, (cuuint64_t)P.p};
         const cuuint64_t strides[1] = {(cuuint64_t)P.L};
-        const cuuint32_t box[2] = {kBoxBytes, 32};
+        const cuuint32_t box[2] = {kBoxBytes, kRowsW};
         const cuuint32_t estr[2] = {1, 1};
         tma = enc && enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(P.in), dims, strides, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -103,13 +134,15 @@ int launch_tiny(const Plan& plan, const MatchParams& P, cudaStream_t s) {
         set_error("no tiny kernel for K=%u B=%u", plan.slots, P.d.sym_bits);
         return PAREM_EINTERNAL;
     }
-    const size_t smem = tiny_smem_bytes(P.d, P.d.sym_bits, tma);
+    MatchParams Q = P;
+    Q.stages = tma ? plan.tma : 0u;
+    const size_t smem = tiny_smem_bytes(P.d, P.d.sym_bits, Q.stages);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
         set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
         return PAREM_ECUDA;
     }
-    void* args[] = {const_cast<MatchParams*>(&P), &map};
+    void* args[] = {&Q, &map};
     e = cudaLaunchKernel(fn, dim3((unsigned)plan.grid), dim3(kT), args, smem, s);
     if (e != cudaSuccess) {
         set_error("tiny kernel launch: %s", cudaGetErrorString(e));

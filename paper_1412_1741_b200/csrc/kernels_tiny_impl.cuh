@@ -13,11 +13,14 @@ namespace parem {
 
 namespace {
 
-constexpr uint32_t kT = kTinyThreads;       // 512 threads = 512 chunks per CTA
+constexpr uint32_t kT = kTinyThreads;       // 512 threads per CTA, one CTA per SM
 constexpr uint32_t kWarps = kT / 32;
-constexpr uint32_t kBoxBytes = 64;          // TMA box: 32 rows x 64 bytes
-constexpr uint32_t kStageBytes = 32 * kBoxBytes;
-constexpr uint32_t kStages = 2;
+constexpr uint32_t kRPL = 2;                // chunks (rows) per lane: two independent chains
+constexpr uint32_t kRowsW = 32 * kRPL;      // rows per warp = rows of one TMA box
+constexpr uint32_t kRows = kT * kRPL;       // chunks per CTA
+constexpr uint32_t kBoxBytes = 64;          // TMA box: 64 rows x 64 bytes = 4 KB
+constexpr uint32_t kStageBytes = kRowsW * kBoxBytes;
+constexpr uint32_t kMaxStages = 3;
 
 __host__ __device__ __forceinline__ size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
 __host__ __device__ __forceinline__ size_t al1k(size_t x) { return (x + 1023) & ~(size_t)1023; }
@@ -27,8 +30,9 @@ struct TinySmem {
 };
 
 // Offsets relative to a 1024-aligned base (the kernel aligns the dynamic smem pointer).
+// `stages` = TMA stages per warp (0: no TMA staging).
 __host__ __device__ __forceinline__ TinySmem tiny_layout(uint32_t Qp, uint32_t Qpad, uint32_t A, uint32_t Lsum_all,
-                                                         uint32_t B, bool tma) {
+                                                         uint32_t B, uint32_t stages) {
     TinySmem s;
     size_t o = 0;
     s.tabk = o;  o += B ? (size_t)Qp * 2048 : 0;
@@ -38,14 +42,15 @@ __host__ __device__ __forceinline__ TinySmem tiny_layout(uint32_t Qp, uint32_t Q
     s.llist = o; o = al16(o + 4 * (size_t)Lsum_all);
     // union: TMA stage buffers during the walk, dense chunk maps afterwards
     s.uni = o = al1k(o);
+    // dense maps of ONE row per lane at a time (the two rows of a lane are composed in turn)
     const size_t maps = al16((size_t)kT * Qpad) + 4 * (size_t)kT * Qpad;
-    const size_t stages = tma ? (size_t)kWarps * kStages * kStageBytes : 0;
+    const size_t stg = (size_t)kWarps * stages * kStageBytes;
     s.mend = s.uni;
     s.mhits = s.uni + al16((size_t)kT * Qpad);
-    o = al16(s.uni + (maps > stages ? maps : stages));
+    o = al16(s.uni + (maps > stg ? maps : stg));
     s.wend = o;  o = al16(o + 4 * (size_t)kWarps * Qpad);
     s.whits = o; o = al16(o + 8 * (size_t)kWarps * Qpad);
-    s.mbar = o;  o = al16(o + 8 * (size_t)kWarps * kStages);
+    s.mbar = o;  o = al16(o + 8 * (size_t)kWarps * kMaxStages);
     s.flag = o;  o = al16(o + 16);
     s.total = o + 1024;   // slack for aligning the dynamic smem base
     return s;
@@ -188,15 +193,50 @@ struct Routes {
     }
 };
 
+// One chunk's A2 data: boundaries [b0, b1), candidate list R_i (Llist[loff .. loff + cnt)),
+// q0 for chunk 0, and |R_i| for the stats (rc).
+struct TinyChunk {
+    uint64_t t, b0, b1;
+    uint32_t cnt, loff, q0, rc;
+    bool live;
+};
+
+__device__ __forceinline__ TinyChunk tiny_chunk(const MatchParams& P, uint64_t t, const uint32_t* Lcnt,
+                                                const uint32_t* Loff) {
+    TinyChunk c;
+    c.t = t;
+    c.live = t < P.p;
+    c.b0 = c.b1 = 0;
+    c.cnt = c.loff = c.q0 = c.rc = 0;
+    if (c.live) {
+        c.b0 = boundary_of(P, t, Lcnt);
+        c.b1 = boundary_of(P, t + 1, Lcnt);
+        if (t == 0) {
+            bool dead;
+            c.q0 = start_state(P, &dead);
+            c.cnt = 1;
+            c.rc = 1;
+        } else {
+            const uint32_t ch = P.in[c.b0 - 1];
+            const uint32_t li = (P.cand == PAREM_CANDIDATES_ENUM || ch >= P.d.A) ? P.d.A : ch;
+            c.cnt = Lcnt[li];
+            c.loff = Loff[li];
+            c.rc = route_count(P, ch, P.in[c.b0], c.cnt);
+        }
+    }
+    return c;
+}
+
 template <int K, int B, bool TMA>
-__global__ void __launch_bounds__(kT) tiny_kernel(const MatchParams P, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     // align the dynamic shared memory base to 1024 B (TMA swizzle atoms)
     unsigned char* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
     const DevDfa& d = P.d;
     const uint32_t Qp = d.Qp, Qpad = d.Qpad, A = d.A;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const TinySmem L = tiny_layout(Qp, Qpad, A, d.Lsum_all, B, TMA);
+    const uint32_t S = TMA ? P.stages : 0u;
+    const TinySmem L = tiny_layout(Qp, Qpad, A, d.Lsum_all, B, S);
     uint32_t* tabk32 = reinterpret_cast<uint32_t*>(sm + L.tabk);
     const unsigned char* tabk = sm + L.tabk;
     uint16_t* tab1 = reinterpret_cast<uint16_t*>(sm + L.tab1);
@@ -208,8 +248,8 @@ __global__ void __launch_bounds__(kT) tiny_kernel(const MatchParams P, const __g
     uint32_t* wend = reinterpret_cast<uint32_t*>(sm + L.wend);
     unsigned long long* whits = reinterpret_cast<unsigned long long*>(sm + L.whits);
     uint32_t* flag = reinterpret_cast<uint32_t*>(sm + L.flag);
-    const uint32_t mbar0 = smem_u32(sm + L.mbar) + warp * kStages * 8u;
-    const uint32_t stage0 = smem_u32(sm + L.uni) + warp * kStages * kStageBytes;
+    const uint32_t mbar0 = smem_u32(sm + L.mbar) + warp * kMaxStages * 8u;
+    const uint32_t stage0 = smem_u32(sm + L.uni) + warp * S * kStageBytes;
 
     // ---- stage the tables (A1 products) into shared memory; init this warp's barriers ----
     if (B)
@@ -220,194 +260,222 @@ __global__ void __launch_bounds__(kT) tiny_kernel(const MatchParams P, const __g
         Loff[i] = __ldg(d.Loff + i);
     }
     for (uint32_t i = tid; i < d.Lsum_all; i += kT) Llist[i] = __ldg(d.Llist + i);
+    const uint64_t row0 = (uint64_t)blockIdx.x * kRows + warp * kRowsW;   // first chunk of this warp
+    const uint32_t nst = TMA ? (uint32_t)(P.L / kBoxBytes) : 0u;
+    const bool warp_live = row0 < P.p;
     if (TMA && lane == 0) {
-        for (uint32_t s = 0; s < kStages; ++s) mbar_init(mbar0 + 8 * s, 1);
+        for (uint32_t s = 0; s < S; ++s) mbar_init(mbar0 + 8 * s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // the first stages do not depend on A2: start streaming before the prologue
+        if (warp_live)
+            for (uint32_t s = 0; s < S && s < nst; ++s) {
+                mbar_expect_tx(mbar0 + 8 * s, kStageBytes);
+                tma_load_2d(stage0 + s * kStageBytes, &tmap, (int32_t)(s * kBoxBytes), (int32_t)row0, mbar0 + 8 * s);
+            }
     }
     __syncthreads();
 
-    // ---- A2: this thread's chunk and its candidate set R_i ----
-    const uint64_t row0 = (uint64_t)blockIdx.x * kT + warp * 32u;   // first chunk of this warp
-    const uint64_t t = row0 + lane;
-    const bool live = t < P.p;
-    uint64_t b0 = 0, b1 = 0;
-    uint32_t cnt = 0, loff = 0, q0 = 0, rc = 0;
-    if (live) {
-        b0 = boundary_of(P, t, Lcnt);
-        b1 = boundary_of(P, t + 1, Lcnt);
-        if (t == 0) {
-            bool dead;
-            q0 = start_state(P, &dead);
-            cnt = 1;
-            rc = 1;
-        } else {
-            const uint32_t c = P.in[b0 - 1];
-            const uint32_t li = (P.cand == PAREM_CANDIDATES_ENUM || c >= A) ? A : c;
-            cnt = Lcnt[li];
-            loff = Loff[li];
-            rc = route_count(P, c, P.in[b0], cnt);
-        }
-    }
+    // ---- A2: this lane's two chunks (rows lane and lane + 32 of the warp's box) and R_i ----
+    const TinyChunk ca = tiny_chunk(P, row0 + lane, Lcnt, Loff);
+    const TinyChunk cb = tiny_chunk(P, row0 + 32 + lane, Lcnt, Loff);
+    const bool act_a = ca.live && ca.cnt, act_b = cb.live && cb.cnt;
     // per-byte invalid bits for A = 1, 2, 4 (powers of two): every bit at or above log2(A)
     const uint32_t bm = B ? (0xFFu & ~(A - 1u)) * 0x01010101u : 0u;
     const uint32_t lane4 = lane << 2;
-    uint32_t badacc = 0;
 
-    // ---- A3 pass 0: the first K candidates, one pass over the chunk ----
-    Routes<K, B> r;
-    r.bad = 0;
-    r.m16 = 16;
-    asm volatile("" : "+r"(r.m16));
+    // ---- A3 pass 0: the first K candidates of both chunks, one pass over the bytes ----
+    Routes<K, B> ra, rb;
+    ra.bad = rb.bad = 0;
+    ra.m16 = 16;
+    asm volatile("" : "+r"(ra.m16));
+    rb.m16 = ra.m16;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        const uint32_t k = cnt ? min((uint32_t)j, cnt - 1) : 0;
-        const uint32_t s = t == 0 ? q0 : (cnt ? Llist[loff + k] : 0u);
-        r.e[j] = B ? ((s << 11) | lane4) : s;
-        r.h[j] = 0;
+        const uint32_t ka = ca.cnt ? min((uint32_t)j, ca.cnt - 1) : 0;
+        const uint32_t kb = cb.cnt ? min((uint32_t)j, cb.cnt - 1) : 0;
+        const uint32_t sa = ca.t == 0 ? ca.q0 : (ca.cnt ? Llist[ca.loff + ka] : 0u);
+        const uint32_t sb = cb.cnt ? Llist[cb.loff + kb] : 0u;
+        ra.e[j] = B ? ((sa << 11) | lane4) : sa;
+        rb.e[j] = B ? ((sb << 11) | lane4) : sb;
+        ra.h[j] = rb.h[j] = 0;
     }
     if (TMA) {
-        // rows [row0, row0 + 32) of the tensor view; every lane walks its own row
-        const uint32_t nst = (uint32_t)(P.L / kBoxBytes);
-        const bool warp_live = row0 < P.p;
-        const uint64_t x0 = t * P.L;                       // nominal start of the row
-        const uint32_t srel = live ? (uint32_t)((b0 - x0 + 15) & ~15ull) : 0xFFFFFFFFu;  // first staged byte used
-        if (live && cnt) r.walk(P.in, b0, min(x0 + srel, b1), tabk, tab1, A, bm, lane4);   // unaligned head
+        const uint64_t xa0 = ca.t * P.L, xb0 = cb.t * P.L;   // nominal row starts
+        // first staged byte each chunk uses (units before it belong to the scalar head)
+        const uint32_t srel_a = act_a ? (uint32_t)((ca.b0 - xa0 + 15) & ~15ull) : 0xFFFFFFFFu;
+        const uint32_t srel_b = act_b ? (uint32_t)((cb.b0 - xb0 + 15) & ~15ull) : 0xFFFFFFFFu;
+        if (act_a) ra.walk(P.in, ca.b0, min(xa0 + srel_a, ca.b1), tabk, tab1, A, bm, lane4);
+        if (act_b) rb.walk(P.in, cb.b0, min(xb0 + srel_b, cb.b1), tabk, tab1, A, bm, lane4);
         if (warp_live) {
-            if (lane == 0)
-                for (uint32_t s = 0; s < kStages && s < nst; ++s) {
-                    mbar_expect_tx(mbar0 + 8 * s, kStageBytes);
-                    tma_load_2d(stage0 + s * kStageBytes, &tmap, (int32_t)(s * kBoxBytes), (int32_t)row0, mbar0 + 8 * s);
-                }
-            // this lane's four 16-byte units of its 64-byte row in a stage (SWIZZLE_64B:
-            // unit u of row l sits at unit u ^ ((l >> 1) & 3))
-            const uint32_t sw = (lane >> 1) & 3u, rowoff = lane * kBoxBytes;
-            const uint32_t o0 = rowoff + ((0u ^ sw) << 4), o1 = rowoff + ((1u ^ sw) << 4),
-                           o2 = rowoff + ((2u ^ sw) << 4), o3 = rowoff + ((3u ^ sw) << 4);
-            const bool act = live && cnt;
+            // SWIZZLE_64B: 16-byte unit u of row l sits at unit u ^ ((l >> 1) & 3); rows l and
+            // l + 32 share the pattern
+            const uint32_t sw = (lane >> 1) & 3u, offa = lane * kBoxBytes, offb = (lane + 32u) * kBoxBytes;
             auto next_stage = [&](uint32_t s, uint32_t slot) {
                 __syncwarp();
-                if (lane == 0 && s + kStages < nst) {
+                if (lane == 0 && s + S < nst) {
                     mbar_expect_tx(mbar0 + 8 * slot, kStageBytes);
-                    tma_load_2d(stage0 + slot * kStageBytes, &tmap, (int32_t)((s + kStages) * kBoxBytes),
-                                (int32_t)row0, mbar0 + 8 * slot);
+                    tma_load_2d(stage0 + slot * kStageBytes, &tmap, (int32_t)((s + S) * kBoxBytes), (int32_t)row0,
+                                mbar0 + 8 * slot);
                 }
             };
-            // advance routes `x` over stage s (units before srel belong to the scalar head;
-            // only stages 0 and 1 can hold such units, so later stages are unguarded)
-            auto run_stage = [&](auto& x, uint32_t s, uint32_t buf) {
-                if (!act) return;
+            // advance both chunks' routes over stage s.  Only stages 0 and 1 can hold head
+            // units (SNAP moves a boundary <= 64 bytes), so later stages run unguarded: an
+            // inactive chunk walks harmless garbage (zero-filled rows past p) and is discarded.
+            auto run_stage = [&](auto& xa, auto& xb, uint32_t s, uint32_t buf) {
                 if (s < 2) {
                     const uint32_t rel = s * kBoxBytes;
-                    if (rel + 0 >= srel) x.vec(lds128(buf + o0), tabk, tab1, A, bm, lane4);
-                    if (rel + 16 >= srel) x.vec(lds128(buf + o1), tabk, tab1, A, bm, lane4);
-                    if (rel + 32 >= srel) x.vec(lds128(buf + o2), tabk, tab1, A, bm, lane4);
-                    if (rel + 48 >= srel) x.vec(lds128(buf + o3), tabk, tab1, A, bm, lane4);
+#pragma unroll 1
+                    for (uint32_t u = 0; u < 4; ++u) {
+                        const uint32_t ou = (u ^ sw) << 4;
+                        if (rel + 16 * u >= srel_a) xa.vec(lds128(buf + offa + ou), tabk, tab1, A, bm, lane4);
+                        if (rel + 16 * u >= srel_b) xb.vec(lds128(buf + offb + ou), tabk, tab1, A, bm, lane4);
+                    }
                 } else {
-                    x.vec(lds128(buf + o0), tabk, tab1, A, bm, lane4);
-                    x.vec(lds128(buf + o1), tabk, tab1, A, bm, lane4);
-                    x.vec(lds128(buf + o2), tabk, tab1, A, bm, lane4);
-                    x.vec(lds128(buf + o3), tabk, tab1, A, bm, lane4);
+#pragma unroll
+                    for (uint32_t u = 0; u < 4; ++u) {
+                        const uint32_t ou = (u ^ sw) << 4;
+                        const uint4 va = lds128(buf + offa + ou);
+                        const uint4 vb = lds128(buf + offb + ou);
+                        xa.vec(va, tabk, tab1, A, bm, lane4);
+                        xb.vec(vb, tabk, tab1, A, bm, lane4);
+                    }
                 }
             };
-            uint32_t s = 0;
+            uint32_t s = 0, slot = 0, phase = 0;
+            auto advance = [&]() {
+                if (++slot == S) {
+                    slot = 0;
+                    phase ^= 1u;
+                }
+                ++s;
+            };
             if constexpr (K > 1) {
                 // Route merging: routes of one chunk that reach the same state stay together
-                // for the rest of the chunk.  Once EVERY lane of the warp has all K routes in
-                // one state (checked per stage, warp-uniform), the warp advances a single
-                // route and rebuilds the others exactly: end = shared end, hits = shared hits
-                // + the per-route offset at the merge point.  Results are unchanged.
-                for (; s < nst; ++s) {
-                    const uint32_t slot = s % kStages;
-                    mbar_wait(mbar0 + 8 * slot, (s / kStages) & 1u);
-                    run_stage(r, s, stage0 + slot * kStageBytes);
+                // for the rest of the chunk.  Once EVERY lane of the warp has all K routes of
+                // both its chunks in one state (checked per stage, warp-uniform), the warp
+                // advances a single route per chunk and rebuilds the others exactly: end =
+                // shared end, hits = shared hits + the per-route offset at the merge point.
+                while (s < nst) {
+                    mbar_wait(mbar0 + 8 * slot, phase);
+                    run_stage(ra, rb, s, stage0 + slot * kStageBytes);
                     next_stage(s, slot);
+                    advance();
                     bool conv = true;
 #pragma unroll
-                    for (int j = 1; j < K; ++j) conv &= r.e[j] == r.e[0];
-                    if (__all_sync(0xFFFFFFFFu, conv || !act)) {
-                        ++s;
-                        break;
-                    }
+                    for (int j = 1; j < K; ++j) conv &= (ra.e[j] == ra.e[0] || !act_a) && (rb.e[j] == rb.e[0] || !act_b);
+                    if (__all_sync(0xFFFFFFFFu, conv)) break;
                 }
                 if (s < nst) {
-                    Routes<1, B> r1;
-                    r1.e[0] = r.e[0];
-                    r1.h[0] = r.h[0];
-                    r1.bad = 0;
-                    r1.m16 = r.m16;
-                    for (; s < nst; ++s) {
-                        const uint32_t slot = s % kStages;
-                        mbar_wait(mbar0 + 8 * slot, (s / kStages) & 1u);
-                        run_stage(r1, s, stage0 + slot * kStageBytes);
+                    Routes<1, B> qa, qb;
+                    qa.e[0] = ra.e[0];
+                    qa.h[0] = ra.h[0];
+                    qb.e[0] = rb.e[0];
+                    qb.h[0] = rb.h[0];
+                    qa.bad = qb.bad = 0;
+                    qa.m16 = qb.m16 = ra.m16;
+                    while (s < nst) {
+                        mbar_wait(mbar0 + 8 * slot, phase);
+                        run_stage(qa, qb, s, stage0 + slot * kStageBytes);
                         next_stage(s, slot);
+                        advance();
                     }
-                    const uint32_t h0 = r.h[0];
+                    const uint32_t ha = ra.h[0], hb = rb.h[0];
 #pragma unroll
                     for (int j = 0; j < K; ++j) {
-                        r.h[j] = r1.h[0] + (r.h[j] - h0);   // u32 wrap-around is exact here
-                        r.e[j] = r1.e[0];
+                        ra.h[j] = qa.h[0] + (ra.h[j] - ha);   // u32 wrap-around is exact here
+                        ra.e[j] = qa.e[0];
+                        rb.h[j] = qb.h[0] + (rb.h[j] - hb);
+                        rb.e[j] = qb.e[0];
                     }
-                    r.bad |= r1.bad;
+                    ra.bad |= qa.bad;
+                    rb.bad |= qb.bad;
                 }
             } else {
-                for (; s < nst; ++s) {
-                    const uint32_t slot = s % kStages;
-                    mbar_wait(mbar0 + 8 * slot, (s / kStages) & 1u);
-                    run_stage(r, s, stage0 + slot * kStageBytes);
+                while (s < nst) {
+                    mbar_wait(mbar0 + 8 * slot, phase);
+                    run_stage(ra, rb, s, stage0 + slot * kStageBytes);
                     next_stage(s, slot);
+                    advance();
                 }
             }
         }
-        if (live && cnt) r.walk(P.in, x0 + P.L, b1, tabk, tab1, A, bm, lane4);   // tail past the row
-    } else if (live && cnt) {
-        r.walk(P.in, b0, b1, tabk, tab1, A, bm, lane4);
+        if (act_a) ra.walk(P.in, xa0 + P.L, ca.b1, tabk, tab1, A, bm, lane4);   // tails past the rows
+        if (act_b) rb.walk(P.in, xb0 + P.L, cb.b1, tabk, tab1, A, bm, lane4);
+    } else {
+        if (act_a) ra.walk(P.in, ca.b0, ca.b1, tabk, tab1, A, bm, lane4);
+        if (act_b) rb.walk(P.in, cb.b0, cb.b1, tabk, tab1, A, bm, lane4);
     }
-    badacc |= r.bad;
     __syncthreads();   // stage buffers are dead from here on: they become the chunk maps
 
-    for (uint32_t q = 0; q < Qpad; ++q) {      // identity map: non-candidates keep their state
-        mend[tid * Qpad + q] = (uint8_t)q;
-        mhits[tid * Qpad + q] = 0;
-    }
-    if (live) {
+    // ---- per-chunk dense maps (identity for non-candidates), extra passes, validation ----
+    auto finish = [&](const TinyChunk& c, Routes<K, B>& r, bool act, uint32_t lr) {
+        for (uint32_t q = 0; q < Qpad; ++q) {
+            mend[lr * Qpad + q] = (uint8_t)q;
+            mhits[lr * Qpad + q] = 0;
+        }
+        if (!c.live) return;
+        uint32_t badacc = act ? r.bad : 0u;
 #pragma unroll
         for (int j = 0; j < K; ++j)
-            if ((uint32_t)j < cnt) {
-                const uint32_t s = t == 0 ? q0 : Llist[loff + j];
-                mend[tid * Qpad + s] = (uint8_t)r.state(j);
-                mhits[tid * Qpad + s] = r.h[j];
+            if ((uint32_t)j < c.cnt) {
+                const uint32_t s = c.t == 0 ? c.q0 : Llist[c.loff + j];
+                mend[lr * Qpad + s] = (uint8_t)r.state(j);
+                mhits[lr * Qpad + s] = r.h[j];
             }
         // extra passes for chunks with more than K candidates (SNAP window miss, Enum)
-        for (uint32_t base = K; base < cnt; base += K) {
+        for (uint32_t base = K; base < c.cnt; base += K) {
             Routes<K, B> x;
             x.bad = 0;
             x.m16 = r.m16;
 #pragma unroll
             for (int j = 0; j < K; ++j) {
-                const uint32_t s = Llist[loff + min(base + (uint32_t)j, cnt - 1)];
+                const uint32_t s = Llist[c.loff + min(base + (uint32_t)j, c.cnt - 1)];
                 x.e[j] = B ? ((s << 11) | lane4) : s;
                 x.h[j] = 0;
             }
-            x.walk(P.in, b0, b1, tabk, tab1, A, bm, lane4);
+            x.walk(P.in, c.b0, c.b1, tabk, tab1, A, bm, lane4);
 #pragma unroll
             for (int j = 0; j < K; ++j)
-                if (base + (uint32_t)j < cnt) {
-                    const uint32_t s = Llist[loff + base + j];
-                    mend[tid * Qpad + s] = (uint8_t)x.state(j);
-                    mhits[tid * Qpad + s] = x.h[j];
+                if (base + (uint32_t)j < c.cnt) {
+                    const uint32_t s = Llist[c.loff + base + j];
+                    mend[lr * Qpad + s] = (uint8_t)x.state(j);
+                    mhits[lr * Qpad + s] = x.h[j];
                 }
         }
-        if (cnt == 0 && first_bad(P.in, b0, b1, A) < b1) badacc = 1;   // R_i empty: still validate
+        if (c.cnt == 0 && first_bad(P.in, c.b0, c.b1, A) < c.b1) badacc = 1;   // R_i empty: still validate
         if (badacc) {
-            const uint64_t off = first_bad(P.in, b0, b1, A);
-            if (off < b1) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
+            const uint64_t off = first_bad(P.in, c.b0, c.b1, A);
+            if (off < c.b1) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
         }
+    };
+    // ---- A4 (first level): each warp composes its 64 chunk maps in row order, lane q =
+    // start state q: rows lane (chunk a) first, then rows 32 + lane (chunk b) ----
+    uint32_t wce = lane < Qpad ? lane : 0;
+    unsigned long long wch = 0;
+    auto compose32 = [&]() {
+        __syncwarp();
+        for (uint32_t i = 0; i < 32; ++i) {
+            const uint32_t row = (warp * 32 + i) * Qpad + wce;
+            const uint32_t ne = mend[row];
+            wch += mhits[row];
+            wce = ne;
+        }
+        __syncwarp();
+    };
+    finish(ca, ra, act_a, warp * 32 + lane);
+    compose32();
+    finish(cb, rb, act_b, warp * 32 + lane);
+    compose32();
+    if (lane < Qpad) {
+        wend[warp * Qpad + lane] = wce;
+        whits[warp * Qpad + lane] = wch;
     }
 
     // ---- stats (warp reduce -> atomics) ----
     {
-        const uint32_t rs = warp_sum(rc);
-        const unsigned long long ss = warp_sum(live ? (unsigned long long)rc * (b1 - b0) : 0ull);
+        const uint32_t rs = warp_sum(ca.rc + cb.rc);
+        const unsigned long long ss = warp_sum((ca.live ? (unsigned long long)ca.rc * (ca.b1 - ca.b0) : 0ull) +
+                                               (cb.live ? (unsigned long long)cb.rc * (cb.b1 - cb.b0) : 0ull));
         if (lane == 0 && rs) {
             atomicAdd(&P.hdr->routes, (unsigned long long)rs);
             atomicAdd(&P.hdr->steps, ss);
@@ -415,22 +483,6 @@ __global__ void __launch_bounds__(kT) tiny_kernel(const MatchParams P, const __g
     }
     __syncthreads();
 
-    // ---- A4: compose the 32 chunk maps of each warp (lane q = start state q) ----
-    {
-        uint32_t ce = lane < Qpad ? lane : 0;
-        unsigned long long ch = 0;
-        for (uint32_t i = 0; i < 32; ++i) {
-            const uint32_t row = (warp * 32 + i) * Qpad + ce;
-            const uint32_t ne = mend[row];
-            ch += mhits[row];
-            ce = ne;
-        }
-        if (lane < Qpad) {
-            wend[warp * Qpad + lane] = ce;
-            whits[warp * Qpad + lane] = ch;
-        }
-    }
-    __syncthreads();
     unsigned long long* tiles = reinterpret_cast<unsigned long long*>(P.maps);
     if (warp == 0) {
         uint32_t ce = lane < Qpad ? lane : 0;

@@ -1,10 +1,11 @@
-// kernels_tiny_inst_b1_t0.cu -- tiny kernel instantiations for B = 1 bits per symbol,
-// TMA staging = false (one TU per (B, TMA) so the build compiles them in parallel).
+// kernels_tiny_inst_b1_t0_0.cu -- tiny kernel instantiations for B = 1 bits per symbol,
+// TMA staging = false, register slots K in {1, 2, 3, 4, 6, 8, 12, 16} (one TU per group so the
+// build compiles the register-unrolled variants in parallel).
 #include "kernels_tiny_impl.cuh"
 
 namespace parem {
 
-const void* tiny_dispatch_b1_t0(uint32_t K) {
+const void* tiny_dispatch_b1_t0_0(uint32_t K) {
     switch (K) {
         case 1: return tiny_fn<1, 1, false>();
         case 2: return tiny_fn<2, 1, false>();

@@ -43,16 +43,16 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
     memset(plan, 0, sizeof(*plan));
     if (!dfa) { set_error("null dfa"); return PAREM_EINVAL; }
     const DevDfa& d = dfa->dev;
-    const uint32_t policy = opts ? opts->boundary_policy : PAREM_BOUNDARY_SNAP;
+    uint32_t policy = opts ? opts->boundary_policy : PAREM_BOUNDARY_AUTO;
     const uint32_t cand = opts ? opts->candidates : PAREM_CANDIDATES_PAREM;
     const uint32_t kreq = opts ? opts->kernel : 0;
     const uint64_t forced = opts ? opts->chunk_len : 0;
-    if (policy > PAREM_BOUNDARY_SNAP) { set_error("bad boundary_policy %u", policy); return PAREM_EINVAL; }
+    if (policy > PAREM_BOUNDARY_AUTO) { set_error("bad boundary_policy %u", policy); return PAREM_EINVAL; }
     if (cand > PAREM_CANDIDATES_ENUM) { set_error("bad candidates %u", cand); return PAREM_EINVAL; }
     if (kreq > kKernelLanes) { set_error("bad kernel %u", kreq); return PAREM_EINVAL; }
-    plan->policy = policy;
     plan->cand = cand;
     if (n == 0) {
+        plan->policy = policy == PAREM_BOUNDARY_AUTO ? PAREM_BOUNDARY_GRID : policy;
         plan->kernel = kKernelTrivial;
         plan->threads = 32;
         plan->grid = 1;
@@ -69,30 +69,36 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         return PAREM_EINVAL;
     }
     plan->kernel = kernel;
+    // AUTO: the thread-per-chunk kernel merges converged routes, so the paper's own GRID
+    // partition costs little extra when every |L(c)| fits the register slots;
+    // SNAP (shorter candidate lists, but boundary scans and unaligned heads) otherwise.
+    if (policy == PAREM_BOUNDARY_AUTO)
+        policy = (kernel == kKernelTiny && d.Lmax <= 8) ? PAREM_BOUNDARY_GRID : PAREM_BOUNDARY_SNAP;
+    plan->policy = policy;
     const int sms = dfa->num_sms > 0 ? dfa->num_sms : 148;
 
     if (kernel == kKernelTiny) {
         const uint32_t B = d.sym_bits;
         uint32_t need = cand == PAREM_CANDIDATES_ENUM ? d.Q : (policy == PAREM_BOUNDARY_SNAP ? d.Lmin : d.Lmax);
         if (need < 1) need = 1;
-        const uint32_t K = tiny_round_slots(need);
-        const bool tma = forced == 0 || forced % 64 == 0;
-        const size_t smem = tiny_smem_bytes(d, B, tma);
-        int bps = cached_bps(1, K, B, tma, kTinyThreads, smem);
+        const uint32_t K = tiny_round_slots(need, B);
+        const uint32_t stages = (forced == 0 || forced % 64 == 0) ? tiny_pick_stages(d, B) : 0u;
+        const size_t smem = tiny_smem_bytes(d, B, stages);
+        int bps = cached_bps(1, K, B, stages, kTinyThreads, smem);
         if (bps <= 0) { set_error("tiny kernel does not fit (smem %zu)", smem); return PAREM_EINVAL; }
         uint64_t L;
         if (forced) L = forced;
         else {
-            const uint64_t target = (uint64_t)sms * bps * kTinyThreads;
+            const uint64_t target = (uint64_t)sms * bps * kTinyThreads * kTinyRowsPerThread;
             L = ceil_div(n, target);
             L = (L + 63) & ~63ull;       // whole TMA boxes per row
             if (L < 256) L = 256;
         }
-        plan->tma = tma;
+        plan->tma = stages;
         if (L > (1ull << 30)) L = 1ull << 30;
         const uint64_t p = n / L ? n / L : 1;
         plan->threads = kTinyThreads;
-        plan->grid = ceil_div(p, kTinyThreads);
+        plan->grid = ceil_div(p, (uint64_t)kTinyThreads * kTinyRowsPerThread);
         plan->p = p;
         plan->L = L;
         plan->slots = K;
