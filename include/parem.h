@@ -81,7 +81,7 @@ typedef struct parem_options {
     uint64_t chunk_len;
     uint32_t boundary_policy;
     uint32_t candidates;
-    uint32_t kernel;       /* 0 = auto; 1 = tiny (thread per chunk); 2 = lanes (CTA per chunk) */
+    uint32_t kernel;       /* 0 = auto; 1 = tiny (thread per chunk); 2 = lanes (group per chunk); 3 = conv (converging: set walk + follow + join) */
     uint32_t reserved[3];
 } parem_options;
 
@@ -157,7 +157,7 @@ typedef struct parem_dfa_info {
 int parem_dfa_get_info(const parem_dfa* dfa, parem_dfa_info* info);
 
 typedef struct parem_plan_info {
-    uint32_t kernel;          /* 1 tiny, 2 lanes                                  */
+    uint32_t kernel;          /* 1 tiny, 2 lanes, 3 conv                          */
     uint32_t block_threads;
     uint64_t grid_blocks;
     uint64_t num_chunks;      /* p                                                */

@@ -18,7 +18,7 @@ from typing import NamedTuple
 import numpy as np
 
 from . import _abi
-from ._abi import (BOUNDARY_AUTO, BOUNDARY_GRID, BOUNDARY_SNAP, CANDIDATES_ENUM, CANDIDATES_PAREM, KERNEL_AUTO, KERNEL_LANES,
+from ._abi import (BOUNDARY_AUTO, BOUNDARY_GRID, BOUNDARY_SNAP, CANDIDATES_ENUM, CANDIDATES_PAREM, KERNEL_AUTO, KERNEL_CONV, KERNEL_LANES,
                    KERNEL_TINY, PAREM_DEAD, PAREM_EINVAL, PAREM_ESYMBOL, PAREM_OK)
 
 __all__ = ["Dfa", "MatchResult", "ParemError", "options", "PAREM_DEAD", "PAREM_OK", "PAREM_ESYMBOL",
@@ -57,7 +57,7 @@ class MatchResult(NamedTuple):
 
 _POLICY = {"grid": BOUNDARY_GRID, "snap": BOUNDARY_SNAP, "auto": BOUNDARY_AUTO}
 _CAND = {"parem": CANDIDATES_PAREM, "enum": CANDIDATES_ENUM}
-_KERNEL = {"auto": KERNEL_AUTO, "tiny": KERNEL_TINY, "lanes": KERNEL_LANES}
+_KERNEL = {"auto": KERNEL_AUTO, "tiny": KERNEL_TINY, "lanes": KERNEL_LANES, "conv": KERNEL_CONV}
 
 
 def options(chunk_len: int = 0, boundary: str = "auto", candidates: str = "parem", kernel: str = "auto"):

@@ -11,7 +11,7 @@ PAREM_OK, PAREM_EINVAL, PAREM_ESYMBOL, PAREM_ECUDA, PAREM_ENOMEM, PAREM_EINTERNA
 PAREM_DEAD = 0xFFFFFFFF
 BOUNDARY_GRID, BOUNDARY_SNAP, BOUNDARY_AUTO = 0, 1, 2
 CANDIDATES_PAREM, CANDIDATES_ENUM = 0, 1
-KERNEL_AUTO, KERNEL_TINY, KERNEL_LANES = 0, 1, 2
+KERNEL_AUTO, KERNEL_TINY, KERNEL_LANES, KERNEL_CONV = 0, 1, 2, 3
 
 
 class parem_result(C.Structure):

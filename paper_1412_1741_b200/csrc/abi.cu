@@ -67,6 +67,7 @@ static int match_impl(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, 
     }
     if (plan.kernel == kKernelTrivial) return launch_trivial(P, stream);
     if (plan.kernel == kKernelTiny) return launch_tiny(plan, P, stream);
+    if (plan.kernel == kKernelConv) return launch_conv(plan, P, stream);
     return launch_lanes(plan, P, stream);
 }
 

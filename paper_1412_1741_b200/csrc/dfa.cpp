@@ -202,6 +202,35 @@ extern "C" int parem_dfa_create(uint32_t Q, uint32_t A, const void* table, uint3
         return PAREM_ECUDA;
     }
 
+    // ---- convergence probe for the converging path (kernels_conv.cu): the set walk
+    // delta*(Q, w) under seeded uniform symbols; how many steps until <= 4 / 1 states ----
+    uint32_t conv_t4 = 0, conv_t1 = 0;
+    if (!tiny && !has_sink) {
+        std::vector<uint32_t> cur(Qp), nxt;
+        std::vector<uint32_t> mark(Qp, 0);
+        for (uint32_t s = 0; s < Qp; ++s) cur[s] = s;
+        uint64_t x = 0x9E3779B97F4A7C15ull;
+        for (uint32_t t = 1; t <= (1u << 16) && cur.size() > 1; ++t) {
+            x += 0x9E3779B97F4A7C15ull;
+            uint64_t z = x;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            z ^= z >> 31;
+            const uint32_t c = (uint32_t)(((unsigned __int128)z * A) >> 64);
+            nxt.clear();
+            for (uint32_t s : cur) {
+                const uint32_t d2 = tab[(size_t)s * A + c];
+                if (mark[d2] != t) {
+                    mark[d2] = t;
+                    nxt.push_back(d2);
+                }
+            }
+            cur.swap(nxt);
+            if (!conv_t4 && cur.size() <= 4) conv_t4 = t;
+            if (cur.size() == 1) conv_t1 = t;
+        }
+    }
+
     parem_dfa* h = new parem_dfa();
     DevDfa& d = h->dev;
     memset(&d, 0, sizeof(d));
@@ -226,6 +255,8 @@ extern "C" int parem_dfa_create(uint32_t Q, uint32_t A, const void* table, uint3
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     h->num_sms = sms;
+    h->conv_t4 = conv_t4;
+    h->conv_t1 = conv_t1;
     *out = h;
     return PAREM_OK;
 }

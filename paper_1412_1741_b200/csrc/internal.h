@@ -27,7 +27,7 @@ constexpr uint32_t kTinyMaxStates = 32;   // dense per-chunk maps live in one wa
 constexpr uint32_t kTinyThreads = 512;    // threads per CTA, tiny kernel
 constexpr uint32_t kTinyRowsPerThread = 2;  // chunks per thread, tiny kernel
 constexpr uint32_t kTinyMaxA = 256;
-constexpr uint32_t kKernelTrivial = 0, kKernelTiny = 1, kKernelLanes = 2;
+constexpr uint32_t kKernelTrivial = 0, kKernelTiny = 1, kKernelLanes = 2, kKernelConv = 3;
 
 struct DevDfa {                // POD, passed by value to every kernel
     uint32_t Q, Qp, Qpad, A;
@@ -46,11 +46,14 @@ struct DevDfa {                // POD, passed by value to every kernel
 
 struct WsHeader {              // first 64 bytes of every workspace (memset to 0 per call)
     unsigned int done;         // CTAs finished (last-CTA detection)
-    unsigned int pad;
+    unsigned int err;          // conv path: internal invariant violated
     unsigned long long bad_inv;  // ~(smallest bad local offset); 0 = none
     unsigned long long routes;   // sum |R_i|
     unsigned long long steps;    // sum |R_i| * len_i
-    unsigned long long pad2[4];
+    unsigned long long hits;     // conv path: total hits along the true path
+    unsigned int final_q;        // conv path: state after the last chunk
+    unsigned int pad;
+    unsigned long long pad2[2];
 };
 static_assert(sizeof(WsHeader) == 64, "header");
 
@@ -99,6 +102,9 @@ struct parem_dfa {
     void* dev_block;
     size_t dev_bytes;
     int num_sms;
+    // create-time convergence probe (set walk from all of Q under seeded uniform symbols):
+    // steps until <= 4 / exactly 1 distinct states remain (0 = not within the probe)
+    uint32_t conv_t4, conv_t1;
 };
 
 namespace parem {
@@ -108,6 +114,9 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
 // device side (kernels_*.cu)
 int launch_tiny(const Plan& plan, const MatchParams& P, cudaStream_t s);
 int launch_lanes(const Plan& plan, const MatchParams& P, cudaStream_t s);
+int launch_conv(const Plan& plan, const MatchParams& P, cudaStream_t s);
+size_t conv_chunk_bytes();
+size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap);
 int launch_trivial(const MatchParams& P, cudaStream_t s);
 int tiny_blocks_per_sm(uint32_t K, uint32_t B, bool tma, size_t smem);
 size_t tiny_smem_bytes(const DevDfa& d, uint32_t B, uint32_t stages);

@@ -1,0 +1,561 @@
+// kernels_conv.cu -- the CONVERGING multi-start path for large DFAs (internal states > 32,
+// complete tables): PaREM's candidate sets R_i are walked with
+// in-flight route merging: routes of one chunk that reach the
+// same state follow the same path for the rest of the chunk (Table II shows it: P_2's
+// routes from 0 and 7 meet after two symbols), so each chunk costs
+// sum_t |delta*(R_i, T[b_i, b_i + t))| lookups instead of |R_i| * len_i.  Results are the
+// sequential ones exactly: the per-chunk map start -> (end, hits) is never approximated,
+// it is evaluated at the one start state the join needs.
+//
+// Four launches per match (all graph-capturable):
+//   K1 conv_set    warp per chunk: walk the SET R_i (deduplicated each step) until at most
+//                  kDMax distinct states remain at offset m_i (or the chunk ends: "open");
+//   K2 conv_follow thread per chunk: walk the <= kDMax survivors z_k over the rest of the
+//                  chunk -> (end_k, tail hits_k); all routes equal at the end = "anchor"
+//                  (the chunk's end state is then independent of its start state);
+//   J  conv_join   one CTA: the true state q_i at every boundary -- q_{i+1} = end of an
+//                  anchor chunk, otherwise walk the head from q_i and pick z_k -- with
+//                  segment-parallel passes (only anchor-free runs are sequential);
+//   K3 conv_heads  thread per chunk: walk q_i over the head [b_i, b_i + m_i) -> z_k and the
+//                  head hits; chunk hits = head + tail_k; last CTA writes the result.
+// Every input byte is read by K2 (tails) or K3 (heads) and validated there (reading C11).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "kernels_common.cuh"
+
+namespace parem {
+
+namespace {
+
+constexpr uint32_t kDMax = 4;             // survivors handed from K1 to K2
+constexpr uint32_t kSetWarps = 8;         // K1: warps (= chunks) per CTA
+constexpr uint32_t kFollowThreads = 512;  // K2 / K3: threads (= chunks) per CTA
+constexpr uint32_t kJoinThreads = 1024;
+
+struct ConvChunk {      // 64 B per chunk in the workspace
+    uint32_t m;         // bytes covered by the set walk (the head)
+    uint32_t D;         // survivors handed over (1..kDMax); 0 = open (head = whole chunk)
+    uint32_t z[kDMax];  // survivor states at b_i + m (padded with z[0])
+    uint32_t end[kDMax];
+    uint32_t tail[kDMax];
+    uint32_t anchor;    // K2: every survivor ended in one state
+    uint32_t q;         // J: true state at b_i
+};
+static_assert(sizeof(ConvChunk) == 64, "ConvChunk");
+
+__host__ __device__ __forceinline__ size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// K1 per-warp scratch: two candidate lists (u16 state indices) and a |Q|-bit image bitmap.
+__host__ __device__ __forceinline__ size_t set_warp_bytes(uint32_t cap, uint32_t Qpad) {
+    return al16(2 * 2 * (size_t)cap) + al16((size_t)(Qpad + 31) / 32 * 4);
+}
+
+__host__ __device__ __forceinline__ size_t tab_bytes(const DevDfa& d) {
+    return (size_t)d.Apad * d.Qpad * (d.lanes_u32 ? 4 : 2);
+}
+
+// Symbol-major table access (entry = dest * ES | acc << (8 ES - 1)): the next entry of a
+// route at entry e under symbol c is at byte offset (e & SMASK) | col(c).
+template <bool SMEM, bool W32>
+struct Tab {
+    static constexpr uint32_t ES = W32 ? 4 : 2, ACC = W32 ? 31 : 15;
+    const unsigned char* g;
+    uint32_t cbase, COL, SMASK, CMASK;
+
+    __device__ __forceinline__ void init(const DevDfa& d, uint32_t sbase) {
+        g = reinterpret_cast<const unsigned char*>(d.lanes_tab);
+        COL = d.Qpad * ES;
+        SMASK = (d.Qpad - 1u) * ES;
+        CMASK = d.Apad - 1u;   // keeps invalid bytes (ESYMBOL) inside the table
+        cbase = SMEM ? sbase : 0u;
+    }
+    __device__ __forceinline__ uint32_t col(uint32_t c) const { return (c & CMASK) * COL + cbase; }
+    __device__ __forceinline__ uint32_t at(uint32_t off) const {
+        uint32_t v;
+        if constexpr (SMEM) {
+            if constexpr (W32) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(off));
+            else asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(off));
+        } else {
+            using ET = typename std::conditional<W32, uint32_t, uint16_t>::type;
+            v = __ldg(reinterpret_cast<const ET*>(g + off));
+        }
+        return v;
+    }
+    __device__ __forceinline__ uint32_t next(uint32_t e, uint32_t colc) const { return at((e & SMASK) | colc); }
+    __device__ __forceinline__ uint32_t state(uint32_t e) const { return (e & SMASK) / ES; }
+    __device__ __forceinline__ uint32_t hit(uint32_t e) const { return e >> ACC; }
+};
+
+// Stage the symbol-major table into shared memory at an address that is a multiple of its
+// column stride (so the shared base ORs into column offsets); returns that address.
+template <bool SMEM, bool W32>
+__device__ __forceinline__ uint32_t stage_table(const DevDfa& d, unsigned char* sm) {
+    if (!SMEM) return 0u;
+    constexpr uint32_t ES = W32 ? 4 : 2;
+    const uint32_t COL = d.Qpad * ES;
+    const uint32_t sraw = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+    const uint32_t sbase = (sraw + COL - 1) / COL * COL;
+    const size_t bytes = tab_bytes(d);
+    const uint4* src = reinterpret_cast<const uint4*>(d.lanes_tab);
+    uint4* dst = reinterpret_cast<uint4*>(sm + (sbase - sraw));
+    for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    return sbase;
+}
+
+__host__ __device__ __forceinline__ size_t smem_tab_bytes(const DevDfa& d, bool smem) {
+    return smem ? al16(tab_bytes(d) + (size_t)d.Qpad * (d.lanes_u32 ? 4 : 2)) : 0;
+}
+
+__device__ __forceinline__ uint64_t conv_b(const MatchParams& P, uint64_t i) {
+    return i >= P.p ? P.n : i * P.L;   // GRID boundaries (reading C7)
+}
+
+// ---------------------------------------------------------------------------------------
+// K1: set walk.  Warp w of the CTA owns chunk t; R_t is deduplicated every step
+// through an image bitmap until <= 32 states remain, then held one per lane (duplicates
+// allowed) and counted with __match_any_sync every 32 bytes until <= kDMax remain.
+template <bool SMEM, bool W32>
+__global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchParams P) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const DevDfa& d = P.d;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t cap = P.slots;   // max |R_i|
+    const size_t tb = smem_tab_bytes(d, SMEM);
+    Tab<SMEM, W32> T;
+    T.init(d, stage_table<SMEM, W32>(d, sm));
+    __syncthreads();
+    unsigned char* ws = sm + tb + warp * set_warp_bytes(cap, d.Qpad);
+    uint16_t* la = reinterpret_cast<uint16_t*>(ws);
+    uint16_t* lb = la + cap;
+    uint32_t* bm = reinterpret_cast<uint32_t*>(ws + al16(4 * (size_t)cap));
+    const uint32_t nbm = (d.Qpad + 31) / 32;
+    const uint64_t t = (uint64_t)blockIdx.x * kSetWarps + warp;
+    if (t >= P.p) return;
+    const uint64_t b0 = conv_b(P, t), b1 = conv_b(P, t + 1);
+    const uint8_t* in = P.in;
+
+    // ---- A2: R_t = L(T[b_t - 1]) (complete tables: S = Q), R_0 = {q0} ----
+    uint32_t D;
+    if (t == 0) {
+        bool dead;
+        D = 1;
+        if (lane == 0) la[0] = (uint16_t)start_state(P, &dead);
+    } else {
+        const uint32_t c = in[b0 - 1];
+        const uint32_t li = (P.cand == PAREM_CANDIDATES_ENUM || c >= d.A) ? d.A : c;
+        D = __ldg(d.Lcnt + li);
+        const uint32_t* list = d.Llist + __ldg(d.Loff + li);
+        for (uint32_t k = lane; k < D; k += 32) la[k] = (uint16_t)__ldg(list + k);
+    }
+    __syncwarp();
+
+    uint64_t pos = b0;
+    uint16_t* cur = la;
+    uint16_t* nxt = lb;
+    const uint32_t ltmask = (1u << lane) - 1u;
+    // ---- phase A: more than 32 states -- deduplicated image every step ----
+    while (D > 32 && pos < b1) {
+        const uint32_t colc = T.col(__ldg(in + pos));
+        for (uint32_t i = lane; i < nbm; i += 32) bm[i] = 0u;
+        __syncwarp();
+        uint32_t nD = 0;
+        for (uint32_t base = 0; base < D; base += 128) {
+            uint32_t ns[4];
+            bool fresh[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t idx = base + 32u * j + lane;
+                ns[j] = idx < D ? T.state(T.next(cur[idx] * T.ES, colc)) : 0xFFFFFFFFu;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                fresh[j] = false;
+                if (ns[j] != 0xFFFFFFFFu) {
+                    const uint32_t bit = 1u << (ns[j] & 31u);
+                    fresh[j] = !(atomicOr(bm + (ns[j] >> 5), bit) & bit);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, fresh[j]);
+                if (fresh[j]) nxt[nD + __popc(bal & ltmask)] = (uint16_t)ns[j];
+                nD += __popc(bal);
+            }
+        }
+        __syncwarp();
+        uint16_t* tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+        D = nD;
+        ++pos;
+    }
+    // ---- phase B: <= 32 states, one per lane (lanes >= D duplicate state cur[0]) ----
+    uint32_t e = (lane < D ? cur[lane] : cur[0]) * T.ES;
+    auto distinct = [&](uint32_t& leaders) {
+        const uint32_t s = T.state(e);
+        const uint32_t m = __match_any_sync(0xFFFFFFFFu, s);
+        leaders = __ballot_sync(0xFFFFFFFFu, (__ffs(m) - 1) == (int)lane);
+        return (uint32_t)__popc(leaders);
+    };
+    uint32_t leaders = 0;
+    uint32_t nd = D > 32 ? D : distinct(leaders);
+    while (nd > kDMax && pos < b1) {
+        // next 32 bytes, one per lane, broadcast by shuffles
+        const uint32_t cnt = (uint32_t)min((uint64_t)32, b1 - pos);
+        const uint32_t mine = lane < cnt ? (uint32_t)__ldg(in + pos + lane) : 0u;
+        for (uint32_t k = 0; k < cnt; ++k) {
+            const uint32_t c = __shfl_sync(0xFFFFFFFFu, mine, k);
+            e = T.next(e, T.col(c));
+        }
+        pos += cnt;
+        nd = distinct(leaders);
+    }
+    ConvChunk* info = reinterpret_cast<ConvChunk*>(P.maps) + t;
+    if (nd > kDMax || D > 32) {   // the set walk reached the chunk end: open chunk
+        if (lane == 0) {
+            info->m = (uint32_t)(b1 - b0);
+            info->D = 0;
+        }
+        return;
+    }
+    // survivors z_0 .. z_{nd-1}: the leader lanes in lane order
+    const uint32_t s = T.state(e);
+    const bool lead = (leaders >> lane) & 1u;
+    const uint32_t r = __popc(leaders & ltmask);
+    const uint32_t s0 = __shfl_sync(0xFFFFFFFFu, s, __ffs(leaders) - 1);
+    if (lead) info->z[r] = s;
+    if (lane >= nd && lane < kDMax) info->z[lane] = s0;
+    if (lane == 0) {
+        info->m = (uint32_t)(pos - b0);
+        info->D = nd;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K2: follow the survivors over the rest of the chunk, thread per chunk, kDMax routes in
+// registers; once every lane of the warp has all its routes in one state (warp-uniform),
+// one route is advanced and the others rebuilt exactly (end shared, hits + offset).
+template <bool SMEM, bool W32>
+__global__ void __launch_bounds__(kFollowThreads) conv_follow_kernel(const MatchParams P) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const DevDfa& d = P.d;
+    Tab<SMEM, W32> T;
+    T.init(d, stage_table<SMEM, W32>(d, sm));
+    __syncthreads();
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = t < P.p;
+    ConvChunk* info = reinterpret_cast<ConvChunk*>(P.maps) + (live ? t : 0);
+    const uint64_t b0 = conv_b(P, t), b1 = live ? conv_b(P, t + 1) : b0;
+    const uint32_t D = live ? info->D : 0u;
+    const bool act = D != 0;
+    uint64_t a = act ? b0 + info->m : b1;
+    uint32_t e[kDMax], h[kDMax];
+#pragma unroll
+    for (int k = 0; k < (int)kDMax; ++k) {
+        e[k] = act ? info->z[k] * T.ES : 0u;
+        h[k] = 0;
+    }
+    const uint8_t* in = P.in;
+    const uint32_t A = d.A;
+    uint32_t bad = 0;
+    auto stepK = [&](uint32_t c) {
+        const uint32_t colc = T.col(c);
+#pragma unroll
+        for (int k = 0; k < (int)kDMax; ++k) {
+            e[k] = T.next(e[k], colc);
+            h[k] += T.hit(e[k]);
+        }
+    };
+    // unaligned head (< 16 bytes)
+    const uint64_t mis = act ? (uint64_t)(((uintptr_t)(in + a)) & 15u) : 0u;
+    uint64_t hd = mis ? a + (16 - mis) : a;
+    if (hd > b1) hd = b1;
+    for (; a < hd; ++a) {
+        const uint32_t c = in[a];
+        bad |= c >= A;
+        stepK(c);
+    }
+    // 16-byte vectors: a warp-uniform trip count (lanes past their own end idle)
+    const uint32_t nv = act ? (uint32_t)((b1 - a) >> 4) : 0u;
+    uint32_t nvmax = nv;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nvmax = max(nvmax, __shfl_xor_sync(0xFFFFFFFFu, nvmax, o));
+    const uint8_t* p = in + a;
+    uint32_t v = 0;
+    for (; v < nvmax; ++v) {
+        if (v < nv) {
+            const uint4 x = ldg_v4(p + 16ull * v);
+            bad |= badbits(x.x, A) | badbits(x.y, A) | badbits(x.z, A) | badbits(x.w, A);
+            const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                stepK(__byte_perm(w4[q], 0u, 0x4440u));
+                stepK(__byte_perm(w4[q], 0u, 0x4441u));
+                stepK(__byte_perm(w4[q], 0u, 0x4442u));
+                stepK(__byte_perm(w4[q], 0u, 0x4443u));
+            }
+        }
+        if ((v & 3u) == 3u) {
+            bool conv = true;
+#pragma unroll
+            for (int k = 1; k < (int)kDMax; ++k) conv &= T.state(e[k]) == T.state(e[0]);
+            if (__all_sync(0xFFFFFFFFu, conv)) {
+                ++v;
+                break;
+            }
+        }
+    }
+    if (v < nvmax) {   // merged: one route per chunk for the rest
+        uint32_t e1 = e[0], h1 = h[0];
+        for (; v < nvmax; ++v) {
+            if (v < nv) {
+                const uint4 x = ldg_v4(p + 16ull * v);
+                bad |= badbits(x.x, A) | badbits(x.y, A) | badbits(x.z, A) | badbits(x.w, A);
+                const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (uint32_t k = 0; k < 4; ++k) {
+                        e1 = T.next(e1, T.col(__byte_perm(w4[q], 0u, 0x4440u | k)));
+                        h1 += T.hit(e1);
+                    }
+            }
+        }
+        const uint32_t h0 = h[0];
+#pragma unroll
+        for (int k = 0; k < (int)kDMax; ++k) {
+            h[k] = h1 + (h[k] - h0);   // u32 wrap-around is exact here
+            e[k] = e1;
+        }
+    }
+    a += (uint64_t)nv << 4;
+    for (; act && a < b1; ++a) {
+        const uint32_t c = in[a];
+        bad |= c >= A;
+        stepK(c);
+    }
+    if (!act) return;
+    bool anchor = true;
+#pragma unroll
+    for (int k = 0; k < (int)kDMax; ++k) {
+        info->end[k] = T.state(e[k]);
+        info->tail[k] = h[k];
+        anchor &= T.state(e[k]) == T.state(e[0]);
+    }
+    info->anchor = anchor;
+    if (bad) {
+        const uint64_t off = first_bad(in, b0 + info->m, b1, A);
+        if (off < b1) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
+    }
+}
+
+// Walk one route from state q over in[a, b) (global table, any alignment); hits optional.
+template <bool W32>
+__device__ __forceinline__ uint32_t walk1(const DevDfa& d, const uint8_t* in, uint64_t a, uint64_t b, uint32_t q,
+                                          uint32_t* hits) {
+    Tab<false, W32> T;
+    T.init(d, 0u);
+    uint32_t e = q * T.ES, h = 0;
+    for (; a < b && (((uintptr_t)(in + a)) & 15u); ++a) {
+        e = T.next(e, T.col(in[a]));
+        h += T.hit(e);
+    }
+    for (; a + 16 <= b; a += 16) {
+        const uint4 x = ldg_v4(in + a);
+        const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2)
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k) {
+                e = T.next(e, T.col(__byte_perm(w4[q2], 0u, 0x4440u | k)));
+                h += T.hit(e);
+            }
+    }
+    for (; a < b; ++a) {
+        e = T.next(e, T.col(in[a]));
+        h += T.hit(e);
+    }
+    if (hits) *hits = h;
+    return T.state(e);
+}
+
+// The state after chunk i given the state q at its start.
+template <bool W32>
+__device__ __forceinline__ uint32_t conv_advance(const MatchParams& P, const ConvChunk* info, uint64_t i, uint32_t q,
+                                                 uint32_t* err) {
+    const ConvChunk& c = info[i];
+    if (c.D != 0 && c.anchor) return c.end[0];
+    const uint64_t b0 = conv_b(P, i);
+    const uint32_t z = walk1<W32>(P.d, P.in, b0, b0 + c.m, q, nullptr);
+    if (c.D == 0) return z;   // open chunk: the head is the whole chunk
+    for (uint32_t k = 0; k < c.D; ++k)
+        if (c.z[k] == z) return c.end[k];
+    *err = 1;   // speculation unsound: the true state is not among the survivors
+    return z;
+}
+
+// ---------------------------------------------------------------------------------------
+// J: the true state at every boundary.  Segment j = chunks [lo_j, hi_j).  Pass 1: exit
+// state of every segment holding an anchor (from its last anchor on); pass 2: one thread
+// chains the segments (an anchor-free segment is walked); pass 3: every segment writes q_i.
+template <bool W32>
+__global__ void __launch_bounds__(kJoinThreads) conv_join_kernel(const MatchParams P) {
+    __shared__ uint32_t sh_has[kJoinThreads], sh_exit[kJoinThreads], sh_in[kJoinThreads];
+    ConvChunk* info = reinterpret_cast<ConvChunk*>(P.maps);
+    const uint32_t j = threadIdx.x;
+    const uint64_t per = (P.p + kJoinThreads - 1) / kJoinThreads;
+    const uint64_t lo = min(P.p, j * per), hi = min(P.p, lo + per);
+    uint32_t err = 0;
+    // pass 1
+    uint64_t la = hi;
+    for (uint64_t i = hi; i > lo; --i)
+        if (info[i - 1].D != 0 && info[i - 1].anchor) {
+            la = i - 1;
+            break;
+        }
+    uint32_t ex = 0;
+    if (la < hi) {
+        ex = info[la].end[0];
+        for (uint64_t i = la + 1; i < hi; ++i) ex = conv_advance<W32>(P, info, i, ex, &err);
+    }
+    sh_has[j] = la < hi;
+    sh_exit[j] = ex;
+    __syncthreads();
+    // pass 2
+    if (j == 0) {
+        bool dead;
+        uint32_t q = start_state(P, &dead);
+        for (uint32_t s = 0; s < kJoinThreads; ++s) {
+            sh_in[s] = q;
+            const uint64_t slo = min(P.p, s * per), shi = min(P.p, slo + per);
+            if (sh_has[s]) q = sh_exit[s];
+            else
+                for (uint64_t i = slo; i < shi; ++i) q = conv_advance<W32>(P, info, i, q, &err);
+        }
+        P.hdr->final_q = q;
+    }
+    __syncthreads();
+    // pass 3
+    uint32_t q = sh_in[j];
+    for (uint64_t i = lo; i < hi; ++i) {
+        info[i].q = q;
+        if (i + 1 < hi) q = conv_advance<W32>(P, info, i, q, &err);
+    }
+    if (err) atomicOr(&P.hdr->err, 1u);
+}
+
+// ---------------------------------------------------------------------------------------
+// K3: the head of every chunk from its true state, the chunk's hits, and the result.
+template <bool W32>
+__global__ void __launch_bounds__(kFollowThreads) conv_heads_kernel(const MatchParams P) {
+    __shared__ unsigned long long acc[3];   // hits, routes, route-steps of this CTA
+    __shared__ uint32_t flag;
+    const DevDfa& d = P.d;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t lane = threadIdx.x & 31u;
+    if (threadIdx.x < 3) acc[threadIdx.x] = 0;
+    __syncthreads();
+    const ConvChunk* info = reinterpret_cast<const ConvChunk*>(P.maps);
+    unsigned long long hits = 0, rc = 0, steps = 0;
+    if (t < P.p) {
+        const ConvChunk& c = info[t];
+        const uint64_t b0 = conv_b(P, t), b1 = conv_b(P, t + 1);
+        uint32_t hh = 0;
+        const uint32_t z = walk1<W32>(d, P.in, b0, b0 + c.m, c.q, &hh);
+        hits = hh;
+        if (c.D != 0) {
+            uint32_t k = 0;
+            while (k < c.D && c.z[k] != z) ++k;
+            if (k == c.D) atomicOr(&P.hdr->err, 1u);
+            else hits += c.tail[k];
+        }
+        const uint64_t off = first_bad(P.in, b0, b0 + c.m, d.A);
+        if (off < b0 + c.m) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
+        // stats: |R_t| (R_0 = {q0}) and |R_t| * len_t
+        if (t == 0) rc = 1;
+        else {
+            const uint32_t cl = P.in[b0 - 1];
+            const uint32_t li = (P.cand == PAREM_CANDIDATES_ENUM || cl >= d.A) ? d.A : cl;
+            rc = route_count(P, cl, P.in[b0], __ldg(d.Lcnt + li));
+        }
+        steps = rc * (b1 - b0);
+    }
+    hits = warp_sum(hits);
+    rc = warp_sum(rc);
+    steps = warp_sum(steps);
+    if (lane == 0) {
+        atomicAdd(acc + 0, hits);
+        atomicAdd(acc + 1, rc);
+        atomicAdd(acc + 2, steps);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicAdd(&P.hdr->hits, acc[0]);
+        atomicAdd(&P.hdr->routes, acc[1]);
+        atomicAdd(&P.hdr->steps, acc[2]);
+        __threadfence();
+        flag = atomicAdd(&P.hdr->done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!flag || threadIdx.x != 0) return;
+    __threadfence();
+    const volatile WsHeader* h = P.hdr;
+    if (h->err) {   // internal invariant violated: report instead of a wrong answer
+        parem_result r;
+        memset(&r, 0, sizeof(r));
+        r.final_state = PAREM_DEAD;
+        r.status = PAREM_EINTERNAL;
+        *P.result = r;
+        return;
+    }
+    bool dead;
+    start_state(P, &dead);
+    write_result(P, h->final_q, h->hits, dead);
+}
+
+template <bool SMEM, bool W32>
+int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
+    const DevDfa& d = P.d;
+    const size_t tb = smem_tab_bytes(d, SMEM);
+    const size_t s1 = tb + kSetWarps * set_warp_bytes(P.slots, d.Qpad);
+    cudaError_t e = cudaFuncSetAttribute(conv_set_kernel<SMEM, W32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(conv_follow_kernel<SMEM, W32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb);
+    if (e != cudaSuccess) {
+        set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+        return PAREM_ECUDA;
+    }
+    const unsigned g1 = (unsigned)((P.p + kSetWarps - 1) / kSetWarps);
+    const unsigned g2 = (unsigned)((P.p + kFollowThreads - 1) / kFollowThreads);
+    conv_set_kernel<SMEM, W32><<<g1, kSetWarps * 32, s1, s>>>(P);
+    conv_follow_kernel<SMEM, W32><<<g2, kFollowThreads, tb, s>>>(P);
+    conv_join_kernel<W32><<<1, kJoinThreads, 0, s>>>(P);
+    conv_heads_kernel<W32><<<g2, kFollowThreads, 0, s>>>(P);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("conv kernels: %s", cudaGetErrorString(e));
+        return PAREM_ECUDA;
+    }
+    return PAREM_OK;
+}
+
+}  // namespace
+
+size_t conv_chunk_bytes() { return sizeof(ConvChunk); }
+
+size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap) {
+    return smem_tab_bytes(d, smem_tab) + kSetWarps * set_warp_bytes(cap, d.Qpad);
+}
+
+int launch_conv(const Plan& plan, const MatchParams& P, cudaStream_t s) {
+    const bool sm = plan.smem_tab != 0, w = P.d.lanes_u32 != 0;
+    if (sm && w) return launch_conv_t<true, true>(plan, P, s);
+    if (sm && !w) return launch_conv_t<true, false>(plan, P, s);
+    if (!sm && w) return launch_conv_t<false, true>(plan, P, s);
+    return launch_conv_t<false, false>(plan, P, s);
+}
+
+}  // namespace parem

@@ -49,7 +49,7 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
     const uint64_t forced = opts ? opts->chunk_len : 0;
     if (policy > PAREM_BOUNDARY_AUTO) { set_error("bad boundary_policy %u", policy); return PAREM_EINVAL; }
     if (cand > PAREM_CANDIDATES_ENUM) { set_error("bad candidates %u", cand); return PAREM_EINVAL; }
-    if (kreq > kKernelLanes) { set_error("bad kernel %u", kreq); return PAREM_EINVAL; }
+    if (kreq > kKernelConv) { set_error("bad kernel %u", kreq); return PAREM_EINVAL; }
     plan->cand = cand;
     if (n == 0) {
         plan->policy = policy == PAREM_BOUNDARY_AUTO ? PAREM_BOUNDARY_GRID : policy;
@@ -59,7 +59,18 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         plan->ws = 256;
         return PAREM_OK;
     }
-    uint32_t kernel = kreq ? kreq : (d.Qp <= kTinyMaxStates ? kKernelTiny : kKernelLanes);
+    // converging path: complete tables whose routes merge (create-time probe), |Q| small
+    // enough for u16 candidate lists and the set walk's per-warp scratch
+    const uint32_t conv_cap = cand == PAREM_CANDIDATES_ENUM ? d.Q : d.Lmax;
+    const bool conv_smem_tab = d.lanes_tab && (size_t)d.Apad * d.Qpad * (d.lanes_u32 ? 4 : 2) <= (size_t)160 * 1024;
+    const bool conv_ok = d.lanes_tab && !d.has_sink && d.Qpad <= 65536 && dfa->conv_t4 > 0 &&
+                         conv_set_smem_bytes(d, conv_smem_tab, conv_cap) <= (size_t)200 * 1024;
+    uint32_t kernel = kreq ? kreq
+                           : (d.Qp <= kTinyMaxStates ? kKernelTiny : (conv_ok ? kKernelConv : kKernelLanes));
+    if (kernel == kKernelConv && !conv_ok) {
+        set_error("converging path needs a complete table of <= 65536 states whose routes merge");
+        return PAREM_EINVAL;
+    }
     if (kernel == kKernelTiny && d.Qp > kTinyMaxStates) {
         set_error("tiny kernel needs <= %u internal states (have %u)", kTinyMaxStates, d.Qp);
         return PAREM_EINVAL;
@@ -109,6 +120,38 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         plan->off_maps = 256;
         plan->ws = al256(plan->off_maps + plan->grid * d.Qpad * 8);
         if (plan->grid > 0x7FFFFFFFull) { set_error("too many chunks"); return PAREM_EINVAL; }
+        return PAREM_OK;
+    }
+
+    if (kernel == kKernelConv) {
+        // K2 runs one thread per chunk: aim for a full wave of them, but keep chunks long
+        // against the set walk's head (~conv_t4 symbols) so K1 stays a small share.
+        uint64_t L;
+        if (forced) L = forced;
+        else {
+            L = ceil_div(n, (uint64_t)sms * 2048);
+            const uint64_t head = 16ull * dfa->conv_t4;
+            if (L < head) L = head;
+            if (L < 4096) L = 4096;
+            L = (L + 15) & ~15ull;
+        }
+        if (L > (1ull << 30)) L = 1ull << 30;
+        const uint64_t p = n / L ? n / L : 1;
+        plan->policy = PAREM_BOUNDARY_GRID;   // the converging path uses the paper's partition
+        plan->threads = 512;
+        plan->grid = ceil_div(p, 512);
+        plan->p = p;
+        plan->L = L;
+        plan->slots = conv_cap;
+        plan->U = 1;
+        plan->sym_per_lookup = 1;
+        plan->win = 0;
+        plan->smem_tab = conv_smem_tab;
+        plan->smem = conv_set_smem_bytes(d, conv_smem_tab, conv_cap);
+        plan->off_maps = 256;
+        plan->off_hits = 0;
+        plan->ws = al256(plan->off_maps + p * conv_chunk_bytes());
+        if (p > 0x7FFFFFFFull) { set_error("too many chunks"); return PAREM_EINVAL; }
         return PAREM_OK;
     }
 

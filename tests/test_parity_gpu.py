@@ -282,3 +282,69 @@ def test_partially_merging_warps(parem, torch_mod, p_reset):
     for b in ("grid", "snap"):
         for L in (0, 4096, 8192 + 64):
             check(parem, torch_mod, t, 0, acc, x, parem.options(boundary=b, chunk_len=L))
+
+
+# ---------------------------------------------------------------- converging path (kernel 3)
+@pytest.mark.parametrize("k", [3, 4, 5])
+@pytest.mark.parametrize("L", [0, 16, 333, 4096, 100000])
+def test_conv_configs(parem, torch_mod, k, L):
+    """Set walk + follow + join + heads (kernels_conv.cu) against the oracle, for chunk
+    lengths from tiny (every chunk open: the join walks them all) to long (anchors), with
+    both candidate rules and an unaligned input view."""
+    c = synth.config(k, n=(1 << 20) + 7)
+    x = c.make_input()
+    for cand in ("parem", "enum"):
+        got = check(parem, torch_mod, c.table, c.start, c.accept, x,
+                    parem.options(chunk_len=L, kernel="conv", candidates=cand), offset=(L + k) % 16)
+        if cand == "parem" and L:
+            b = oracle.grid_boundaries(x.size, L)
+            assert got.num_chunks == len(b) - 1
+            assert (got.routes, got.route_steps) == oracle.route_stats(c.table, x, b)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_conv_random_dfas(parem, torch_mod, seed):
+    """Random complete DFAs (33..2000 states, any alphabet) on the converging path, with
+    random chunk lengths and start states; start states may be accepting."""
+    rng = np.random.default_rng(9000 + seed)
+    Q = int(rng.choice([33, 40, 100, 256, 600, 2000]))
+    A = int(rng.choice([2, 3, 4, 26, 200, 256]))
+    t = synth.random_dfa(Q, A, int(rng.integers(0, 1 << 30)), np.uint16 if seed % 2 else np.uint32)
+    acc = rng.random(Q) < float(rng.choice([0.05, 0.5, 0.95]))
+    q0 = int(rng.integers(0, Q))
+    with parem.Dfa(t, q0, acc) as d:
+        if d.plan(1 << 20)["kernel"] != 3:
+            pytest.skip("routes of this DFA do not merge within the probe")
+    n = int(rng.choice([1, 17, 4095, 100003, 1 << 20]))
+    x = rng.integers(0, A, n).astype(np.uint8)
+    L = int(rng.choice([0, 0, 1, 50, 1000, 30000]))
+    check(parem, torch_mod, t, q0, acc, x, parem.options(chunk_len=L, kernel="conv"), offset=seed % 16)
+
+
+def test_conv_rejects_non_merging_dfa(parem, torch_mod):
+    """A permutation DFA never merges routes: auto picks the lanes kernel and forcing the
+    converging path is an EINVAL, not a wrong answer."""
+    Q, A = 64, 4
+    t = np.array([[(q + c + 1) % Q for c in range(A)] for q in range(Q)], dtype=np.uint16)
+    acc = np.zeros(Q, dtype=bool)
+    acc[5] = True
+    with parem.Dfa(t, 0, acc) as d:
+        assert d.plan(1 << 20)["kernel"] == 2
+        with pytest.raises(parem.ParemError):
+            d.match(to_dev(torch_mod, np.zeros(100, np.uint8)), parem.options(kernel="conv"))
+    x = synth.uniform_symbols(300001, A, seed=64)
+    check(parem, torch_mod, t, 0, acc, x)
+
+
+def test_conv_symbol_errors(parem, torch_mod):
+    """ESYMBOL with the smallest offset whether the bad byte sits in a head (K3) or a tail
+    (K2) of the converging path."""
+    c = synth.config(3, n=1 << 20)
+    rng = np.random.default_rng(3)
+    for L in (0, 64, 5000):
+        for trial in range(3):
+            x = c.make_input().copy()
+            bad = np.sort(rng.integers(0, x.size, 2))
+            x[bad] = 200
+            got = check(parem, torch_mod, c.table, c.start, c.accept, x, parem.options(chunk_len=L, kernel="conv"))
+            assert got.status == parem.PAREM_ESYMBOL and got.bad_offset == bad[0]
