@@ -33,7 +33,6 @@ namespace {
 constexpr uint32_t kDMax = 4;             // survivors handed from K1 to K2
 constexpr uint32_t kSetWarps = 8;         // K1: warps (= chunks) per CTA
 constexpr uint32_t kFollowThreads = 512;  // K2 / K3: threads (= chunks) per CTA
-constexpr uint32_t kJoinThreads = 1024;
 
 struct ConvChunk {      // 64 B per chunk in the workspace
     uint32_t m;         // bytes covered by the set walk (the head)
@@ -132,10 +131,10 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
     uint16_t* lb = la + cap;
     uint32_t* bm = reinterpret_cast<uint32_t*>(ws + al16(4 * (size_t)cap));
     const uint32_t nbm = (d.Qpad + 31) / 32;
-    const uint64_t t = (uint64_t)blockIdx.x * kSetWarps + warp;
-    if (t >= P.p) return;
-    const uint64_t b0 = conv_b(P, t), b1 = conv_b(P, t + 1);
     const uint8_t* in = P.in;
+    // persistent warps: the table is staged once per CTA, chunks are strided over warps
+    for (uint64_t t = (uint64_t)blockIdx.x * kSetWarps + warp; t < P.p; t += (uint64_t)gridDim.x * kSetWarps) {
+    const uint64_t b0 = conv_b(P, t), b1 = conv_b(P, t + 1);
 
     // ---- A2: R_t = L(T[b_t - 1]) (complete tables: S = Q), R_0 = {q0} ----
     uint32_t D;
@@ -219,7 +218,8 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
             info->m = (uint32_t)(b1 - b0);
             info->D = 0;
         }
-        return;
+        __syncwarp();
+        continue;
     }
     // survivors z_0 .. z_{nd-1}: the leader lanes in lane order
     const uint32_t s = T.state(e);
@@ -232,12 +232,45 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
         info->m = (uint32_t)(pos - b0);
         info->D = nd;
     }
+    __syncwarp();
+    }
 }
 
 // ---------------------------------------------------------------------------------------
-// K2: follow the survivors over the rest of the chunk, thread per chunk, kDMax routes in
-// registers; once every lane of the warp has all its routes in one state (warp-uniform),
-// one route is advanced and the others rebuilt exactly (end shared, hits + offset).
+// K2: follow the survivors over the rest of the chunk, thread per chunk, K routes in
+// registers with K = the warp's largest survivor count (1, 2 or 4); once every lane of the
+// warp has all its routes in one state (warp-uniform), one route is advanced and the
+// others rebuilt exactly (end shared, hits + the offset at the merge point).
+template <int K, bool SMEM, bool W32>
+__device__ __forceinline__ uint32_t follow_vecs(const Tab<SMEM, W32>& T, const uint8_t* p, uint32_t v, uint32_t nv,
+                                                uint32_t nvmax, uint32_t A, uint32_t* e, uint32_t* h, uint32_t& bad) {
+    for (; v < nvmax; ++v) {
+        if (v < nv) {
+            const uint4 x = ldg_v4(p + 16ull * v);
+            bad |= badbits(x.x, A) | badbits(x.y, A) | badbits(x.z, A) | badbits(x.w, A);
+            const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (uint32_t b = 0; b < 4; ++b) {
+                    const uint32_t colc = T.col(__byte_perm(w4[q], 0u, 0x4440u | b));
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        e[k] = T.next(e[k], colc);
+                        h[k] += T.hit(e[k]);
+                    }
+                }
+        }
+        if (K > 1 && (v & 3u) == 3u) {
+            bool conv = true;
+#pragma unroll
+            for (int k = 1; k < K; ++k) conv &= T.state(e[k]) == T.state(e[0]);
+            if (__all_sync(0xFFFFFFFFu, conv)) return v + 1;
+        }
+    }
+    return v;
+}
+
 template <bool SMEM, bool W32>
 __global__ void __launch_bounds__(kFollowThreads) conv_follow_kernel(const MatchParams P) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -278,57 +311,28 @@ __global__ void __launch_bounds__(kFollowThreads) conv_follow_kernel(const Match
         bad |= c >= A;
         stepK(c);
     }
-    // 16-byte vectors: a warp-uniform trip count (lanes past their own end idle)
+    // 16-byte vectors: a warp-uniform trip count (lanes past their own end idle) and a
+    // warp-uniform route count
     const uint32_t nv = act ? (uint32_t)((b1 - a) >> 4) : 0u;
-    uint32_t nvmax = nv;
+    uint32_t nvmax = nv, Dw = D;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nvmax = max(nvmax, __shfl_xor_sync(0xFFFFFFFFu, nvmax, o));
+    for (int o = 16; o > 0; o >>= 1) {
+        nvmax = max(nvmax, __shfl_xor_sync(0xFFFFFFFFu, nvmax, o));
+        Dw = max(Dw, __shfl_xor_sync(0xFFFFFFFFu, Dw, o));
+    }
     const uint8_t* p = in + a;
     uint32_t v = 0;
-    for (; v < nvmax; ++v) {
-        if (v < nv) {
-            const uint4 x = ldg_v4(p + 16ull * v);
-            bad |= badbits(x.x, A) | badbits(x.y, A) | badbits(x.z, A) | badbits(x.w, A);
-            const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+    if (Dw > 2) v = follow_vecs<4>(T, p, v, nv, nvmax, A, e, h, bad);
+    else if (Dw == 2) v = follow_vecs<2>(T, p, v, nv, nvmax, A, e, h, bad);
+    if (v < nvmax) {   // one route per chunk for the rest; rebuild the others exactly
+        const uint32_t e0 = e[0], h0 = h[0];
+        v = follow_vecs<1>(T, p, v, nv, nvmax, A, e, h, bad);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                stepK(__byte_perm(w4[q], 0u, 0x4440u));
-                stepK(__byte_perm(w4[q], 0u, 0x4441u));
-                stepK(__byte_perm(w4[q], 0u, 0x4442u));
-                stepK(__byte_perm(w4[q], 0u, 0x4443u));
+        for (int k = 1; k < (int)kDMax; ++k) {
+            if (Dw > 1 || T.state(e[k]) == T.state(e0)) {
+                h[k] = h[0] + (h[k] - h0);   // u32 wrap-around is exact here
+                e[k] = e[0];
             }
-        }
-        if ((v & 3u) == 3u) {
-            bool conv = true;
-#pragma unroll
-            for (int k = 1; k < (int)kDMax; ++k) conv &= T.state(e[k]) == T.state(e[0]);
-            if (__all_sync(0xFFFFFFFFu, conv)) {
-                ++v;
-                break;
-            }
-        }
-    }
-    if (v < nvmax) {   // merged: one route per chunk for the rest
-        uint32_t e1 = e[0], h1 = h[0];
-        for (; v < nvmax; ++v) {
-            if (v < nv) {
-                const uint4 x = ldg_v4(p + 16ull * v);
-                bad |= badbits(x.x, A) | badbits(x.y, A) | badbits(x.z, A) | badbits(x.w, A);
-                const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-#pragma unroll
-                    for (uint32_t k = 0; k < 4; ++k) {
-                        e1 = T.next(e1, T.col(__byte_perm(w4[q], 0u, 0x4440u | k)));
-                        h1 += T.hit(e1);
-                    }
-            }
-        }
-        const uint32_t h0 = h[0];
-#pragma unroll
-        for (int k = 0; k < (int)kDMax; ++k) {
-            h[k] = h1 + (h[k] - h0);   // u32 wrap-around is exact here
-            e[k] = e1;
         }
     }
     a += (uint64_t)nv << 4;
@@ -398,51 +402,55 @@ __device__ __forceinline__ uint32_t conv_advance(const MatchParams& P, const Con
 }
 
 // ---------------------------------------------------------------------------------------
-// J: the true state at every boundary.  Segment j = chunks [lo_j, hi_j).  Pass 1: exit
-// state of every segment holding an anchor (from its last anchor on); pass 2: one thread
-// chains the segments (an anchor-free segment is walked); pass 3: every segment writes q_i.
+// J: the true state q_i at every boundary (the join).  Thread per chunk:
+// q_i = end of the nearest anchor chunk a < i (its end does not depend on its start),
+// advanced through the non-anchor chunks a+1 .. i-1 (head walk + survivor pick).  A chunk
+// with no anchor among its kJoinBack predecessors is left to conv_join_seq_kernel, which
+// runs the whole chain on one thread only when some chunk needed it.
+constexpr uint32_t kJoinBack = 32;
+constexpr uint32_t kUnresolved = 0xFFFFFFFFu;
+
 template <bool W32>
-__global__ void __launch_bounds__(kJoinThreads) conv_join_kernel(const MatchParams P) {
-    __shared__ uint32_t sh_has[kJoinThreads], sh_exit[kJoinThreads], sh_in[kJoinThreads];
+__global__ void __launch_bounds__(kFollowThreads) conv_join_kernel(const MatchParams P) {
     ConvChunk* info = reinterpret_cast<ConvChunk*>(P.maps);
-    const uint32_t j = threadIdx.x;
-    const uint64_t per = (P.p + kJoinThreads - 1) / kJoinThreads;
-    const uint64_t lo = min(P.p, j * per), hi = min(P.p, lo + per);
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.p) return;
+    uint32_t err = 0, q = kUnresolved;
+    uint64_t a = i;   // first chunk to advance through
+    bool dead;
+    if (i == 0) q = start_state(P, &dead);
+    else {
+        const uint64_t lo = i > kJoinBack ? i - kJoinBack : 0;
+        for (uint64_t j = i; j > lo; --j) {
+            const ConvChunk& c = info[j - 1];
+            if (c.D != 0 && c.anchor) {
+                q = c.end[0];
+                a = j;
+                break;
+            }
+        }
+        if (q == kUnresolved && lo == 0) {   // no anchor back to chunk 0: start from q0
+            q = start_state(P, &dead);
+            a = 0;
+        }
+    }
+    if (q == kUnresolved) atomicOr(&P.hdr->err, 2u);   // chain too long: sequential pass
+    else
+        for (uint64_t j = a; j < i; ++j) q = conv_advance<W32>(P, info, j, q, &err);
+    info[i].q = q;
+    if (err) atomicOr(&P.hdr->err, 1u);
+}
+
+template <bool W32>
+__global__ void conv_join_seq_kernel(const MatchParams P) {
+    if (threadIdx.x != 0 || !(P.hdr->err & 2u)) return;
+    ConvChunk* info = reinterpret_cast<ConvChunk*>(P.maps);
     uint32_t err = 0;
-    // pass 1
-    uint64_t la = hi;
-    for (uint64_t i = hi; i > lo; --i)
-        if (info[i - 1].D != 0 && info[i - 1].anchor) {
-            la = i - 1;
-            break;
-        }
-    uint32_t ex = 0;
-    if (la < hi) {
-        ex = info[la].end[0];
-        for (uint64_t i = la + 1; i < hi; ++i) ex = conv_advance<W32>(P, info, i, ex, &err);
-    }
-    sh_has[j] = la < hi;
-    sh_exit[j] = ex;
-    __syncthreads();
-    // pass 2
-    if (j == 0) {
-        bool dead;
-        uint32_t q = start_state(P, &dead);
-        for (uint32_t s = 0; s < kJoinThreads; ++s) {
-            sh_in[s] = q;
-            const uint64_t slo = min(P.p, s * per), shi = min(P.p, slo + per);
-            if (sh_has[s]) q = sh_exit[s];
-            else
-                for (uint64_t i = slo; i < shi; ++i) q = conv_advance<W32>(P, info, i, q, &err);
-        }
-        P.hdr->final_q = q;
-    }
-    __syncthreads();
-    // pass 3
-    uint32_t q = sh_in[j];
-    for (uint64_t i = lo; i < hi; ++i) {
+    bool dead;
+    uint32_t q = start_state(P, &dead);
+    for (uint64_t i = 0; i < P.p; ++i) {
         info[i].q = q;
-        if (i + 1 < hi) q = conv_advance<W32>(P, info, i, q, &err);
+        q = conv_advance<W32>(P, info, i, q, &err);
     }
     if (err) atomicOr(&P.hdr->err, 1u);
 }
@@ -466,12 +474,17 @@ __global__ void __launch_bounds__(kFollowThreads) conv_heads_kernel(const MatchP
         uint32_t hh = 0;
         const uint32_t z = walk1<W32>(d, P.in, b0, b0 + c.m, c.q, &hh);
         hits = hh;
+        uint32_t fin = z;   // open chunk: the head is the whole chunk
         if (c.D != 0) {
             uint32_t k = 0;
             while (k < c.D && c.z[k] != z) ++k;
             if (k == c.D) atomicOr(&P.hdr->err, 1u);
-            else hits += c.tail[k];
+            else {
+                hits += c.tail[k];
+                fin = c.end[k];
+            }
         }
+        if (t == P.p - 1) P.hdr->final_q = fin;
         const uint64_t off = first_bad(P.in, b0, b0 + c.m, d.A);
         if (off < b0 + c.m) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
         // stats: |R_t| (R_0 = {q0}) and |R_t| * len_t
@@ -503,7 +516,7 @@ __global__ void __launch_bounds__(kFollowThreads) conv_heads_kernel(const MatchP
     if (!flag || threadIdx.x != 0) return;
     __threadfence();
     const volatile WsHeader* h = P.hdr;
-    if (h->err) {   // internal invariant violated: report instead of a wrong answer
+    if (h->err & 1u) {   // internal invariant violated: report instead of a wrong answer
         parem_result r;
         memset(&r, 0, sizeof(r));
         r.final_state = PAREM_DEAD;
@@ -528,11 +541,18 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
         set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
         return PAREM_ECUDA;
     }
-    const unsigned g1 = (unsigned)((P.p + kSetWarps - 1) / kSetWarps);
+    int bps = 0, sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, conv_set_kernel<SMEM, W32>, kSetWarps * 32, s1);
+    if (bps < 1) bps = 1;
+    uint64_t g1w = (P.p + kSetWarps - 1) / kSetWarps;
+    const unsigned g1 = (unsigned)(g1w < (uint64_t)sms * bps ? g1w : (uint64_t)sms * bps);
     const unsigned g2 = (unsigned)((P.p + kFollowThreads - 1) / kFollowThreads);
     conv_set_kernel<SMEM, W32><<<g1, kSetWarps * 32, s1, s>>>(P);
     conv_follow_kernel<SMEM, W32><<<g2, kFollowThreads, tb, s>>>(P);
-    conv_join_kernel<W32><<<1, kJoinThreads, 0, s>>>(P);
+    conv_join_kernel<W32><<<g2, kFollowThreads, 0, s>>>(P);
+    conv_join_seq_kernel<W32><<<1, 32, 0, s>>>(P);
     conv_heads_kernel<W32><<<g2, kFollowThreads, 0, s>>>(P);
     e = cudaGetLastError();
     if (e != cudaSuccess) {
