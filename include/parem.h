@@ -82,8 +82,16 @@ typedef struct parem_options {
     uint32_t boundary_policy;
     uint32_t candidates;
     uint32_t kernel;       /* 0 = auto; 1 = tiny (thread per chunk); 2 = lanes (group per chunk); 3 = conv (converging: set walk + follow + join) */
-    uint32_t reserved[3];
+    uint32_t flags;        /* PAREM_FLAG_* */
+    uint32_t reserved[2];
 } parem_options;
+
+/* flags: the workspace's 64-byte header is already zero -- freshly zero-filled by the
+ * caller, or left so by a previous call on it that completed (every completed call leaves
+ * it zeroed, ESYMBOL and EINTERNAL results included).  The library then skips its per-call
+ * header reset (one cudaMemsetAsync), so a match is exactly its kernel launches.  Without
+ * the flag the header is reset on `stream` before the kernels. */
+#define PAREM_FLAG_WS_CLEAN 1u
 
 typedef struct parem_dfa parem_dfa;
 
@@ -178,6 +186,22 @@ const char* parem_last_error(void);
 
 /* Version string. */
 const char* parem_version(void);
+
+/* ---- per-kernel timing (bench.py; off by default) ----
+ * parem_profile(1) clears the record and makes every later match issued by this host
+ * thread record CUDA events on its stream around each kernel it launches (not while the
+ * stream is being captured into a graph); parem_profile(0) stops recording.
+ * parem_profile_read() waits for the events and returns one entry per recorded kernel
+ * launch, in launch order: kernel name, device duration (ms) and the index of its match
+ * since parem_profile(1); *count = number of entries (<= max are written).
+ * Returns PAREM_OK or PAREM_ECUDA. */
+typedef struct parem_kernel_time {
+    char name[40];
+    float ms;
+    uint32_t match;
+} parem_kernel_time;
+int parem_profile(int enable);
+int parem_profile_read(parem_kernel_time* out, int max, int* count);
 
 /* ---- roofline micro-benchmarks (bench.py; not part of the matching path) ----
  * Each returns the device time in milliseconds of `reps` back-to-back launches measured

@@ -21,8 +21,8 @@ from . import _abi
 from ._abi import (BOUNDARY_AUTO, BOUNDARY_GRID, BOUNDARY_SNAP, CANDIDATES_ENUM, CANDIDATES_PAREM, KERNEL_AUTO, KERNEL_CONV, KERNEL_LANES,
                    KERNEL_TINY, PAREM_DEAD, PAREM_EINVAL, PAREM_ESYMBOL, PAREM_OK)
 
-__all__ = ["Dfa", "MatchResult", "ParemError", "options", "PAREM_DEAD", "PAREM_OK", "PAREM_ESYMBOL",
-           "PAREM_EINVAL", "lib"]
+__all__ = ["Dfa", "MatchResult", "ParemError", "options", "profile", "profile_read", "PAREM_DEAD", "PAREM_OK",
+           "PAREM_ESYMBOL", "PAREM_EINVAL", "lib"]
 
 
 def lib():
@@ -60,13 +60,37 @@ _CAND = {"parem": CANDIDATES_PAREM, "enum": CANDIDATES_ENUM}
 _KERNEL = {"auto": KERNEL_AUTO, "tiny": KERNEL_TINY, "lanes": KERNEL_LANES, "conv": KERNEL_CONV}
 
 
-def options(chunk_len: int = 0, boundary: str = "auto", candidates: str = "parem", kernel: str = "auto"):
+def options(chunk_len: int = 0, boundary: str = "auto", candidates: str = "parem", kernel: str = "auto",
+            ws_clean: bool = False):
+    """parem_options.  ``ws_clean`` sets PAREM_FLAG_WS_CLEAN: the workspace header is known
+    to be zero (torch.zeros, or a previous completed call), so no per-call reset is issued."""
     o = _abi.parem_options()
     o.chunk_len = int(chunk_len)
     o.boundary_policy = _POLICY[boundary]
     o.candidates = _CAND[candidates]
     o.kernel = _KERNEL[kernel]
+    o.flags = _abi.FLAG_WS_CLEAN if ws_clean else 0
     return o
+
+
+def profile(enable: bool = True) -> None:
+    """parem_profile: record CUDA events around every kernel of later matches (this thread)."""
+    lib().parem_profile(1 if enable else 0)
+
+
+def profile_read() -> list[tuple[int, str, float]]:
+    """(match index, kernel name, device ms) for every kernel launch recorded since
+    profile(True), in launch order."""
+    L = lib()
+    n = C.c_int(0)
+    st = L.parem_profile_read(None, 0, C.byref(n))
+    if st != PAREM_OK:
+        _err(L, st)
+    buf = (_abi.parem_kernel_time * max(1, n.value))()
+    st = L.parem_profile_read(buf, n.value, C.byref(n))
+    if st != PAREM_OK:
+        _err(L, st)
+    return [(int(buf[i].match), buf[i].name.decode(), float(buf[i].ms)) for i in range(n.value)]
 
 
 def _err(L, status: int):

@@ -22,7 +22,14 @@ class parem_result(C.Structure):
 
 class parem_options(C.Structure):
     _fields_ = [("chunk_len", C.c_uint64), ("boundary_policy", C.c_uint32), ("candidates", C.c_uint32),
-                ("kernel", C.c_uint32), ("reserved", C.c_uint32 * 3)]
+                ("kernel", C.c_uint32), ("flags", C.c_uint32), ("reserved", C.c_uint32 * 2)]
+
+
+FLAG_WS_CLEAN = 1
+
+
+class parem_kernel_time(C.Structure):
+    _fields_ = [("name", C.c_char * 40), ("ms", C.c_float), ("match", C.c_uint32)]
 
 
 class parem_dfa_info(C.Structure):
@@ -45,7 +52,8 @@ assert C.sizeof(parem_options) == 32
 EXPORTS = [
     "parem_dfa_create", "parem_dfa_destroy", "parem_workspace_bytes", "parem_match_async",
     "parem_match_continue_async", "parem_match", "parem_match_host", "parem_dfa_get_info", "parem_plan",
-    "parem_last_error", "parem_version", "parem_bench_read_stream", "parem_bench_gather",
+    "parem_last_error", "parem_version", "parem_bench_read_stream", "parem_bench_gather", "parem_profile",
+    "parem_profile_read",
 ]
 
 _LIB = None
@@ -76,6 +84,10 @@ def load(path: str = SO_PATH):
     L.parem_match.argtypes = [vp, vp, u64, O, R, vp]
     L.parem_match_host.restype = i32
     L.parem_match_host.argtypes = [vp, vp, u64, O, R, vp]
+    L.parem_profile.restype = i32
+    L.parem_profile.argtypes = [i32]
+    L.parem_profile_read.restype = i32
+    L.parem_profile_read.argtypes = [C.POINTER(parem_kernel_time), i32, C.POINTER(i32)]
     L.parem_dfa_get_info.restype = i32
     L.parem_dfa_get_info.argtypes = [vp, C.POINTER(parem_dfa_info)]
     L.parem_plan.restype = i32

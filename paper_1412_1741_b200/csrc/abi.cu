@@ -4,6 +4,9 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <string>
+#include <vector>
+
 #include "kernels_common.cuh"
 
 namespace parem {
@@ -19,12 +22,66 @@ __global__ void trivial_kernel(const MatchParams P) {
 
 int launch_trivial(const MatchParams& P, cudaStream_t s) {
     trivial_kernel<<<1, 32, 0, s>>>(P);
+    prof_after("trivial", s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_error("trivial kernel: %s", cudaGetErrorString(e));
         return PAREM_ECUDA;
     }
     return PAREM_OK;
+}
+
+// ---- per-kernel timing (parem_profile) ----
+namespace {
+struct ProfRec {
+    cudaEvent_t start, stop;
+    std::string name;
+    uint32_t match;
+};
+struct ProfState {
+    bool on = false;
+    bool active = false;        // the current match records events
+    cudaEvent_t last = nullptr; // event after the previous kernel of the current match
+    uint32_t matches = 0;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<ProfRec> recs;
+};
+thread_local ProfState g_prof;
+
+cudaEvent_t prof_event() {
+    ProfState& p = g_prof;
+    if (p.used == p.pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        p.pool.push_back(e);
+    }
+    return p.pool[p.used++];
+}
+
+void prof_begin(cudaStream_t s) {
+    ProfState& p = g_prof;
+    p.active = false;
+    if (!p.on) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    cudaEvent_t e = prof_event();
+    if (!e) return;
+    cudaEventRecord(e, s);
+    p.last = e;
+    p.active = true;
+    ++p.matches;
+}
+}  // namespace
+
+void prof_after(const char* name, cudaStream_t s) {
+    ProfState& p = g_prof;
+    if (!p.active) return;
+    cudaEvent_t e = prof_event();
+    if (!e) return;
+    cudaEventRecord(e, s);
+    p.recs.push_back(ProfRec{p.last, e, name, p.matches - 1});
+    p.last = e;
 }
 
 static int match_impl(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, uint64_t offset_base, void* d_ws,
@@ -60,11 +117,14 @@ static int match_impl(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, 
     P.hdr = reinterpret_cast<WsHeader*>(d_ws);
     P.maps = reinterpret_cast<char*>(d_ws) + plan.off_maps;
     P.map_hits = plan.off_hits ? reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(d_ws) + plan.off_hits) : nullptr;
-    cudaError_t e = cudaMemsetAsync(d_ws, 0, sizeof(WsHeader), stream);
-    if (e != cudaSuccess) {
-        set_error("cudaMemsetAsync: %s", cudaGetErrorString(e));
-        return PAREM_ECUDA;
+    if (!(opts && (opts->flags & PAREM_FLAG_WS_CLEAN))) {
+        cudaError_t e = cudaMemsetAsync(d_ws, 0, sizeof(WsHeader), stream);
+        if (e != cudaSuccess) {
+            set_error("cudaMemsetAsync: %s", cudaGetErrorString(e));
+            return PAREM_ECUDA;
+        }
     }
+    prof_begin(stream);
     if (plan.kernel == kKernelTrivial) return launch_trivial(P, stream);
     if (plan.kernel == kKernelTiny) return launch_tiny(plan, P, stream);
     if (plan.kernel == kKernelConv) return launch_conv(plan, P, stream);
@@ -263,6 +323,38 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint16_t* __restrict_
 }
 
 }  // namespace parem
+
+extern "C" int parem_profile(int enable) {
+    ProfState& p = g_prof;
+    if (enable) {
+        p.used = 0;
+        p.recs.clear();
+        p.matches = 0;
+    }
+    p.on = enable != 0;
+    p.active = false;
+    return PAREM_OK;
+}
+
+extern "C" int parem_profile_read(parem_kernel_time* out, int max, int* count) {
+    ProfState& p = g_prof;
+    const int nk = (int)p.recs.size();
+    if (count) *count = nk;
+    for (int k = 0; k < nk && k < max; ++k) {
+        const ProfRec& r = p.recs[k];
+        if (cudaEventSynchronize(r.stop) != cudaSuccess) {
+            set_error("parem_profile_read: event sync failed");
+            return PAREM_ECUDA;
+        }
+        float ms = 0;
+        cudaEventElapsedTime(&ms, r.start, r.stop);
+        memset(out[k].name, 0, sizeof(out[k].name));
+        strncpy(out[k].name, r.name.c_str(), sizeof(out[k].name) - 1);
+        out[k].ms = ms;
+        out[k].match = r.match;
+    }
+    return PAREM_OK;
+}
 
 extern "C" float parem_bench_read_stream(const uint8_t* d_input, uint64_t n, uint32_t* d_sink, int reps,
                                          void* stream_) {

@@ -108,8 +108,10 @@ struct parem_dfa {
 };
 
 namespace parem {
-// host side (dfa.cpp / planner.cpp)
+// host side (dfa.cpp / planner.cpp / abi.cu)
 void set_error(const char* fmt, ...);
+// per-kernel timing (parem_profile): call after each kernel launch of a match
+void prof_after(const char* name, cudaStream_t s);
 int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan* plan);
 // device side (kernels_*.cu)
 int launch_tiny(const Plan& plan, const MatchParams& P, cudaStream_t s);

@@ -99,6 +99,20 @@ __device__ __forceinline__ uint64_t first_bad(const uint8_t* in, uint64_t a, uin
     return b;
 }
 
+// Every completed match leaves its workspace header zeroed (PAREM_FLAG_WS_CLEAN): the
+// last CTA calls this after reading the header.
+__device__ __forceinline__ void reset_header(const MatchParams& P) {
+    volatile WsHeader* h = P.hdr;
+    h->done = 0;
+    h->err = 0;
+    h->bad_inv = 0;
+    h->routes = 0;
+    h->steps = 0;
+    h->hits = 0;
+    h->final_q = 0;
+    __threadfence();
+}
+
 // Epilogue, run by one thread of the last CTA: q is the internal state reached from the
 // start state, hits the matches counted on that path (u64).
 __device__ __forceinline__ void write_result(const MatchParams& P, uint32_t q, unsigned long long hits,
@@ -136,7 +150,7 @@ __device__ __forceinline__ void write_result(const MatchParams& P, uint32_t q, u
         r.bad_offset = 0;
     }
     *P.result = r;
-    h->done = 0;   // the header is re-zeroed per call anyway; keep it tidy
+    reset_header(P);
 }
 
 template <typename T>

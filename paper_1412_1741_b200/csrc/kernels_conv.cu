@@ -522,6 +522,7 @@ __global__ void __launch_bounds__(kFollowThreads) conv_heads_kernel(const MatchP
         r.final_state = PAREM_DEAD;
         r.status = PAREM_EINTERNAL;
         *P.result = r;
+        reset_header(P);
         return;
     }
     bool dead;
@@ -550,10 +551,15 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     const unsigned g1 = (unsigned)(g1w < (uint64_t)sms * bps ? g1w : (uint64_t)sms * bps);
     const unsigned g2 = (unsigned)((P.p + kFollowThreads - 1) / kFollowThreads);
     conv_set_kernel<SMEM, W32><<<g1, kSetWarps * 32, s1, s>>>(P);
+    prof_after("conv_set", s);
     conv_follow_kernel<SMEM, W32><<<g2, kFollowThreads, tb, s>>>(P);
+    prof_after("conv_follow", s);
     conv_join_kernel<W32><<<g2, kFollowThreads, 0, s>>>(P);
+    prof_after("conv_join", s);
     conv_join_seq_kernel<W32><<<1, 32, 0, s>>>(P);
+    prof_after("conv_join_seq", s);
     conv_heads_kernel<W32><<<g2, kFollowThreads, 0, s>>>(P);
+    prof_after("conv_heads", s);
     e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_error("conv kernels: %s", cudaGetErrorString(e));

@@ -308,6 +308,7 @@ int launch_lanes(const Plan& plan, const MatchParams& P, cudaStream_t s) {
         set_error("lanes kernel launch: %s", cudaGetErrorString(e));
         return PAREM_ECUDA;
     }
+    prof_after("lanes", s);
     return PAREM_OK;
 }
 

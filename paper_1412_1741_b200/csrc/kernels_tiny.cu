@@ -148,6 +148,7 @@ int launch_tiny(const Plan& plan, const MatchParams& P, cudaStream_t s) {
         set_error("tiny kernel launch: %s", cudaGetErrorString(e));
         return PAREM_ECUDA;
     }
+    prof_after("tiny", s);
     return PAREM_OK;
 }
 

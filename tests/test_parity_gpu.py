@@ -348,3 +348,45 @@ def test_conv_symbol_errors(parem, torch_mod):
             x[bad] = 200
             got = check(parem, torch_mod, c.table, c.start, c.accept, x, parem.options(chunk_len=L, kernel="conv"))
             assert got.status == parem.PAREM_ESYMBOL and got.bad_offset == bad[0]
+
+
+# ---------------------------------------------------------------- clean-workspace contract
+@pytest.mark.parametrize("k,kernel", [(1, "auto"), (2, "auto"), (3, "conv"), (3, "lanes"), (5, "conv")])
+def test_ws_clean_reuse(parem, torch_mod, k, kernel):
+    """PAREM_FLAG_WS_CLEAN: a zero-filled workspace reused across calls without any reset --
+    every completed call (ESYMBOL included) must leave the header zeroed for the next."""
+    torch = torch_mod
+    c = synth.config(k, n=300_007)
+    rng = np.random.default_rng(k)
+    with parem.Dfa(c.table, c.start, c.accept) as d:
+        opts = parem.options(kernel=kernel, ws_clean=True)
+        ws = torch.zeros(d.workspace_bytes(c.n, opts), dtype=torch.uint8, device="cuda")
+        res = torch.zeros(64, dtype=torch.uint8, device="cuda")
+        for trial in range(6):
+            x = c.make_input().copy()
+            if trial % 3 == 1 and c.A < 256:
+                x[int(rng.integers(0, x.size))] = 255
+            x = x[: x.size - 1000 * trial]
+            ref = oracle.walk(c.table, c.start, c.accept, x)
+            d.match_async(to_dev(torch, x), ws, res, opts)
+            got = parem.MatchResult.from_bytes(res.cpu().numpy().tobytes()[:56])
+            if ref.status == oracle.ESYMBOL:
+                assert got.status == parem.PAREM_ESYMBOL and got.bad_offset == ref.bad_offset
+            else:
+                assert got.status == 0 and (got.final_state, got.accepted, got.match_count) == \
+                    (ref.final_state, ref.accepted, ref.match_count), (trial, got, ref)
+            assert not ws[:64].any(), "header not left zeroed"
+
+
+def test_profile_records_kernels(parem, torch_mod):
+    c = synth.config(3, n=1 << 20)
+    with parem.Dfa(c.table, c.start, c.accept) as d:
+        xd = to_dev(torch_mod, c.make_input())
+        parem.profile(True)
+        d.match(xd)
+        d.match(xd)
+        parem.profile(False)
+        recs = parem.profile_read()
+    names = [r[1] for r in recs]
+    assert names == ["conv_set", "conv_follow", "conv_join", "conv_join_seq", "conv_heads"] * 2
+    assert {r[0] for r in recs} == {0, 1} and all(r[2] > 0 for r in recs)
