@@ -17,6 +17,8 @@
 //     one LOP3, one LDS, one LEA.HI per group and route;
 //   * tab1[s][c] = dest | acc << 15 for single-symbol steps (unaligned heads and tails) and
 //     for the generic path (A > 4).
+#include <stdlib.h>
+
 #include "kernels_tiny_impl.cuh"
 
 namespace parem {
@@ -86,9 +88,9 @@ size_t tiny_smem_bytes(const DevDfa& d, uint32_t B, uint32_t stages) {
     return tiny_layout(d.Qp, d.Qpad, d.A, d.Lsum_all, B, stages).total;
 }
 
-// TMA stages per warp: as many 4 KB boxes (<= kMaxStages) as fit next to the tables in one
-// CTA's opt-in shared memory; 0 = no TMA staging.  More than ~48 boxes in flight per SM
-// collapses TMA throughput (profiles/r01_stream_probe.txt), so 16 warps x 3 is the cap.
+// TMA stages per warp: two 4 KB boxes (16 warps x 2 = 32 boxes in flight per SM; more than
+// ~48 collapses TMA throughput and 3 stages measured 1.8% slower on cfg2,
+// profiles/r01_stream_probe.txt), fewer if the tables leave no room; 0 = no TMA staging.
 uint32_t tiny_pick_stages(const DevDfa& d, uint32_t B) {
     static int limit = 0;
     if (!limit) {
@@ -98,7 +100,12 @@ uint32_t tiny_pick_stages(const DevDfa& d, uint32_t B) {
             v = 232448;
         limit = v;
     }
-    for (uint32_t s = kMaxStages; s >= 2; --s)
+    uint32_t smax = 2;
+    if (const char* e = getenv("PAREM_TINY_STAGES")) {   // experiments only (2 or 3)
+        const int v = atoi(e);
+        if (v >= 2 && v <= (int)kMaxStages) smax = (uint32_t)v;
+    }
+    for (uint32_t s = smax; s >= 2; --s)
         if (tiny_smem_bytes(d, B, s) <= (size_t)limit) return s;
     return 0;
 }
