@@ -66,6 +66,7 @@ struct MatchParams {
     uint32_t policy, cand, win, slots;
     uint32_t tg;               // lanes: threads per chunk group
     uint32_t stages;           // tiny: TMA stages per warp (0 = no TMA)
+    uint32_t dmax;             // conv: survivors handed from the set walk to the follow walk
     uint64_t offset_base;
     const parem_result* carry; // may be null
     parem_result* result;
@@ -85,6 +86,7 @@ struct Plan {
     uint32_t win;
     uint32_t smem_tab;       // lanes: table staged in shared memory
     uint32_t tma;            // tiny: TMA stages per warp (0 = rows read with 16-B loads)
+    uint32_t dmax;           // conv: set-walk hand-over threshold (1, 2 or 4 survivors)
     size_t smem;
     size_t ws;
     size_t off_maps, off_hits;

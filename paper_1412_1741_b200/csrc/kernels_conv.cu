@@ -201,7 +201,8 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
     };
     uint32_t leaders = 0;
     uint32_t nd = D > 32 ? D : distinct(leaders);
-    while (nd > kDMax && pos < b1) {
+    const uint32_t dmax = P.dmax;
+    while (nd > dmax && pos < b1) {
         // next 32 bytes, one per lane, broadcast by shuffles
         const uint32_t cnt = (uint32_t)min((uint64_t)32, b1 - pos);
         const uint32_t mine = lane < cnt ? (uint32_t)__ldg(in + pos + lane) : 0u;
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
         nd = distinct(leaders);
     }
     ConvChunk* info = reinterpret_cast<ConvChunk*>(P.maps) + t;
-    if (nd > kDMax || D > 32) {   // the set walk reached the chunk end: open chunk
+    if (nd > dmax || D > 32) {   // the set walk reached the chunk end: open chunk
         if (lane == 0) {
             info->m = (uint32_t)(b1 - b0);
             info->D = 0;
@@ -244,9 +245,13 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
 template <int K, bool SMEM, bool W32>
 __device__ __forceinline__ uint32_t follow_vecs(const Tab<SMEM, W32>& T, const uint8_t* p, uint32_t v, uint32_t nv,
                                                 uint32_t nvmax, uint32_t A, uint32_t* e, uint32_t* h, uint32_t& bad) {
+    // the next 16 bytes are loaded while the current ones are walked (one vector in flight
+    // per thread hides the HBM latency behind the dependent lookups)
+    uint4 nx = v < nv ? ldg_v4(p + 16ull * v) : make_uint4(0, 0, 0, 0);
     for (; v < nvmax; ++v) {
+        const uint4 x = nx;
+        if (v + 1 < nv) nx = ldg_v4(p + 16ull * (v + 1));
         if (v < nv) {
-            const uint4 x = ldg_v4(p + 16ull * v);
             bad |= badbits(x.x, A) | badbits(x.y, A) | badbits(x.z, A) | badbits(x.w, A);
             const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -367,8 +372,10 @@ __device__ __forceinline__ uint32_t walk1(const DevDfa& d, const uint8_t* in, ui
         e = T.next(e, T.col(in[a]));
         h += T.hit(e);
     }
+    uint4 nx = a + 16 <= b ? ldg_v4(in + a) : make_uint4(0, 0, 0, 0);
     for (; a + 16 <= b; a += 16) {
-        const uint4 x = ldg_v4(in + a);
+        const uint4 x = nx;
+        if (a + 32 <= b) nx = ldg_v4(in + a + 16);
         const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
         for (int q2 = 0; q2 < 4; ++q2)
@@ -407,7 +414,7 @@ __device__ __forceinline__ uint32_t conv_advance(const MatchParams& P, const Con
 // advanced through the non-anchor chunks a+1 .. i-1 (head walk + survivor pick).  A chunk
 // with no anchor among its kJoinBack predecessors is left to conv_join_seq_kernel, which
 // runs the whole chain on one thread only when some chunk needed it.
-constexpr uint32_t kJoinBack = 32;
+constexpr uint32_t kJoinBack = 128;
 constexpr uint32_t kUnresolved = 0xFFFFFFFFu;
 
 template <bool W32>

@@ -9,6 +9,7 @@
 //     max_c |L(c)| (W_exec <= W_grid; results are partition-invariant);
 //   * slots (registers per thread, or lanes per CTA) are sized for the expected |R_i|;
 //     a chunk with more candidates runs extra passes over its bytes.
+#include <stdlib.h>
 #include <string.h>
 
 #include <map>
@@ -127,17 +128,30 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         // K2 runs one thread per chunk: aim for a full wave of them, but keep chunks long
         // against the set walk's head (~conv_t4 symbols) so K1 stays a small share.
         uint64_t L;
+        // K2 runs one thread per chunk; 512 per SM measured best on cfg3/cfg5 (fewer chunks =
+        // less set-walk work, enough chains to keep the lookups in flight)
+        uint64_t chains = (uint64_t)sms * 512;
+        uint32_t dmax = 4;
+        if (const char* e = getenv("PAREM_CONV_CHAINS")) chains = strtoull(e, nullptr, 10);   // experiments
+        if (const char* e = getenv("PAREM_CONV_DMAX")) dmax = (uint32_t)atoi(e);
+        if ((dmax != 1 && dmax != 2) || dfa->conv_t1 == 0) dmax = 4;
         if (forced) L = forced;
         else {
-            L = ceil_div(n, (uint64_t)sms * 2048);
-            const uint64_t head = 16ull * dfa->conv_t4;
+            L = ceil_div(n, chains ? chains : 1);
+            // chunks >= 16x the probe's convergence length, so open chunks (no hand-over,
+            // resolved by head walks in the join) stay rare
+            const uint64_t head = 16ull * (dmax == 4 ? dfa->conv_t4 : dfa->conv_t1);
             if (L < head) L = head;
             if (L < 4096) L = 4096;
             L = (L + 15) & ~15ull;
+            // thread-per-chunk 16-B load streams at a stride that is a multiple of 128 B run
+            // ~18% slower (profiles/r01_stride_probe.txt): shift such strides by 16 B
+            if (L % 128 == 0) L += 16;
         }
         if (L > (1ull << 30)) L = 1ull << 30;
         const uint64_t p = n / L ? n / L : 1;
         plan->policy = PAREM_BOUNDARY_GRID;   // the converging path uses the paper's partition
+        plan->dmax = dmax;
         plan->threads = 512;
         plan->grid = ceil_div(p, 512);
         plan->p = p;

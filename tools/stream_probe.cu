@@ -244,6 +244,21 @@ int main(int argc, char** argv) {
     float ms = timeit(launch_coal, &c, reps);
     printf("coalesced          %8.1f GB/s\n", n / ms / 1e6);
 
+    if (argc > 1 && argv[1][0] == 'L') {
+        // stride sweep: thread-per-chunk ldg streams (75776 threads) and TMA row boxes (tiny geometry)
+        for (uint64_t Lf = 13824; Lf <= 13824 + 352; Lf += 16) {
+            Ctx x = c;
+            x.fn = (const void*)ldg_chunk<4>;
+            x.block = 512;
+            x.grid = sms;
+            uint64_t T = (uint64_t)x.grid * 512;
+            x.L = Lf;
+            x.smem = 0;
+            float t = timeit(launch_generic, &x, reps);
+            printf("ldg  L=%llu (mod256=%llu) %8.1f GB/s\n", (unsigned long long)Lf, (unsigned long long)(Lf % 256),
+                   (double)(x.L * T) / t / 1e6);
+        }
+    }
     auto run_ldg = [&](const void* fn, const char* name, int block, int per_sm) {
         Ctx x = c;
         x.fn = fn;
@@ -345,6 +360,14 @@ int main(int argc, char** argv) {
     run_tma2((const void*)tma_rows2<256, 2, 32>, "t2<256,2,32> 128x3", 256, 2, 32, 128, 3, P256);
     run_tma2((const void*)tma_rows2<256, 2, 16>, "t2<256,2,16> 256x3", 256, 2, 16, 256, 3, P256);
     run_tma2((const void*)tma_rows2<512, 2, 8>, "t2<512,2,8> 256x3", 512, 2, 8, 256, 3, P256);
+    if (argc > 1 && argv[1][0] == 'L') {
+        for (uint64_t Lf = 6784; Lf <= 7072; Lf += 16) {
+            char nm[64];
+            snprintf(nm, 64, "tma L=%llu (mod256=%llu)", (unsigned long long)Lf, (unsigned long long)(Lf % 256));
+            run_tma2((const void*)tma_rows2<64, 2, 64>, nm, 64, 2, 64, 512, 1, P256, Lf);
+        }
+        return 0;
+    }
     if (argc > 1) {
         run_tma2((const void*)tma_rows2<64, 2, 32>, "t2<64,2,32> 256x3", 64, 2, 32, 256, 3, P256);
         run_tma2((const void*)tma_rows2<64, 3, 32>, "t2<64,3,32> 256x3", 64, 3, 32, 256, 3, P256);
