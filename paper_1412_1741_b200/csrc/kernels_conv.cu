@@ -47,9 +47,10 @@ static_assert(sizeof(ConvChunk) == 64, "ConvChunk");
 
 __host__ __device__ __forceinline__ size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
 
-// K1 per-warp scratch: two candidate lists (u16 state indices) and a |Q|-bit image bitmap.
+// K1 per-warp scratch: the candidate list (u16 state indices, compacted in place) and a
+// |Q|-bit image bitmap.
 __host__ __device__ __forceinline__ size_t set_warp_bytes(uint32_t cap, uint32_t Qpad) {
-    return al16(2 * 2 * (size_t)cap) + al16((size_t)(Qpad + 31) / 32 * 4);
+    return al16(2 * (size_t)cap) + al16((size_t)(Qpad + 31) / 32 * 4);
 }
 
 __host__ __device__ __forceinline__ size_t tab_bytes(const DevDfa& d) {
@@ -113,9 +114,14 @@ __device__ __forceinline__ uint64_t conv_b(const MatchParams& P, uint64_t i) {
 }
 
 // ---------------------------------------------------------------------------------------
-// K1: set walk.  Warp w of the CTA owns chunk t; R_t is deduplicated every step
-// through an image bitmap until <= 32 states remain, then held one per lane (duplicates
-// allowed) and counted with __match_any_sync every 32 bytes until <= kDMax remain.
+// K1: set walk.  Persistent warps take chunks in turn; R_t is deduplicated every step
+// through an image bitmap (phase A) until <= 32 states remain.  The chunk is then PARKED in
+// one of kPark register slots (one state per lane, duplicates allowed) and the warp
+// advances all its parked chunks together, 32 bytes at a time -- kPark independent lookup
+// chains per lane -- counting distinct states with __match_any_sync, until <= dmax remain
+// (hand-over) or the chunk ends (open).  A freed slot is refilled by the next chunk's phase A.
+constexpr int kPark = 4;
+
 template <bool SMEM, bool W32>
 __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchParams P) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -127,113 +133,157 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
     T.init(d, stage_table<SMEM, W32>(d, sm));
     __syncthreads();
     unsigned char* ws = sm + tb + warp * set_warp_bytes(cap, d.Qpad);
-    uint16_t* la = reinterpret_cast<uint16_t*>(ws);
-    uint16_t* lb = la + cap;
-    uint32_t* bm = reinterpret_cast<uint32_t*>(ws + al16(4 * (size_t)cap));
+    uint16_t* list = reinterpret_cast<uint16_t*>(ws);   // compacted in place
+    uint32_t* bm = reinterpret_cast<uint32_t*>(ws + al16(2 * (size_t)cap));
     const uint32_t nbm = (d.Qpad + 31) / 32;
     const uint8_t* in = P.in;
-    // persistent warps: the table is staged once per CTA, chunks are strided over warps
-    for (uint64_t t = (uint64_t)blockIdx.x * kSetWarps + warp; t < P.p; t += (uint64_t)gridDim.x * kSetWarps) {
-    const uint64_t b0 = conv_b(P, t), b1 = conv_b(P, t + 1);
-
-    // ---- A2: R_t = L(T[b_t - 1]) (complete tables: S = Q), R_0 = {q0} ----
-    uint32_t D;
-    if (t == 0) {
-        bool dead;
-        D = 1;
-        if (lane == 0) la[0] = (uint16_t)start_state(P, &dead);
-    } else {
-        const uint32_t c = in[b0 - 1];
-        const uint32_t li = (P.cand == PAREM_CANDIDATES_ENUM || c >= d.A) ? d.A : c;
-        D = __ldg(d.Lcnt + li);
-        const uint32_t* list = d.Llist + __ldg(d.Loff + li);
-        for (uint32_t k = lane; k < D; k += 32) la[k] = (uint16_t)__ldg(list + k);
-    }
-    __syncwarp();
-
-    uint64_t pos = b0;
-    uint16_t* cur = la;
-    uint16_t* nxt = lb;
     const uint32_t ltmask = (1u << lane) - 1u;
-    // ---- phase A: more than 32 states -- deduplicated image every step ----
-    while (D > 32 && pos < b1) {
-        const uint32_t colc = T.col(__ldg(in + pos));
-        for (uint32_t i = lane; i < nbm; i += 32) bm[i] = 0u;
-        __syncwarp();
-        uint32_t nD = 0;
-        for (uint32_t base = 0; base < D; base += 128) {
-            uint32_t ns[4];
-            bool fresh[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t idx = base + 32u * j + lane;
-                ns[j] = idx < D ? T.state(T.next(cur[idx] * T.ES, colc)) : 0xFFFFFFFFu;
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                fresh[j] = false;
-                if (ns[j] != 0xFFFFFFFFu) {
-                    const uint32_t bit = 1u << (ns[j] & 31u);
-                    fresh[j] = !(atomicOr(bm + (ns[j] >> 5), bit) & bit);
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, fresh[j]);
-                if (fresh[j]) nxt[nD + __popc(bal & ltmask)] = (uint16_t)ns[j];
-                nD += __popc(bal);
-            }
-        }
-        __syncwarp();
-        uint16_t* tmp = cur;
-        cur = nxt;
-        nxt = tmp;
-        D = nD;
-        ++pos;
-    }
-    // ---- phase B: <= 32 states, one per lane (lanes >= D duplicate state cur[0]) ----
-    uint32_t e = (lane < D ? cur[lane] : cur[0]) * T.ES;
-    auto distinct = [&](uint32_t& leaders) {
-        const uint32_t s = T.state(e);
-        const uint32_t m = __match_any_sync(0xFFFFFFFFu, s);
+    const uint32_t dmax = P.dmax;
+    ConvChunk* infos = reinterpret_cast<ConvChunk*>(P.maps);
+
+    auto distinct = [&](uint32_t e, uint32_t& leaders) {
+        const uint32_t m = __match_any_sync(0xFFFFFFFFu, T.state(e));
         leaders = __ballot_sync(0xFFFFFFFFu, (__ffs(m) - 1) == (int)lane);
         return (uint32_t)__popc(leaders);
     };
-    uint32_t leaders = 0;
-    uint32_t nd = D > 32 ? D : distinct(leaders);
-    const uint32_t dmax = P.dmax;
-    while (nd > dmax && pos < b1) {
-        // next 32 bytes, one per lane, broadcast by shuffles
-        const uint32_t cnt = (uint32_t)min((uint64_t)32, b1 - pos);
-        const uint32_t mine = lane < cnt ? (uint32_t)__ldg(in + pos + lane) : 0u;
-        for (uint32_t k = 0; k < cnt; ++k) {
-            const uint32_t c = __shfl_sync(0xFFFFFFFFu, mine, k);
-            e = T.next(e, T.col(c));
-        }
-        pos += cnt;
-        nd = distinct(leaders);
-    }
-    ConvChunk* info = reinterpret_cast<ConvChunk*>(P.maps) + t;
-    if (nd > dmax || D > 32) {   // the set walk reached the chunk end: open chunk
+    auto write_open = [&](uint64_t t, uint64_t b0, uint64_t b1) {
         if (lane == 0) {
-            info->m = (uint32_t)(b1 - b0);
-            info->D = 0;
+            infos[t].m = (uint32_t)(b1 - b0);
+            infos[t].D = 0;
         }
-        __syncwarp();
-        continue;
-    }
-    // survivors z_0 .. z_{nd-1}: the leader lanes in lane order
-    const uint32_t s = T.state(e);
-    const bool lead = (leaders >> lane) & 1u;
-    const uint32_t r = __popc(leaders & ltmask);
-    const uint32_t s0 = __shfl_sync(0xFFFFFFFFu, s, __ffs(leaders) - 1);
-    if (lead) info->z[r] = s;
-    if (lane >= nd && lane < kDMax) info->z[lane] = s0;
-    if (lane == 0) {
-        info->m = (uint32_t)(pos - b0);
-        info->D = nd;
-    }
-    __syncwarp();
+    };
+    // survivors z_0 .. z_{nd-1}: the leader lanes in lane order, padded with z_0
+    auto write_handover = [&](uint64_t t, uint64_t m, uint32_t e, uint32_t leaders, uint32_t nd) {
+        const uint32_t s = T.state(e);
+        const uint32_t s0 = __shfl_sync(0xFFFFFFFFu, s, __ffs(leaders) - 1);
+        if ((leaders >> lane) & 1u) infos[t].z[__popc(leaders & ltmask)] = s;
+        if (lane >= nd && lane < kDMax) infos[t].z[lane] = s0;
+        if (lane == 0) {
+            infos[t].m = (uint32_t)m;
+            infos[t].D = nd;
+        }
+    };
+
+    uint64_t pt[kPark], ppos[kPark], pb0[kPark], pb1[kPark];
+    uint32_t pe[kPark];
+    uint32_t occ = 0;   // occupied slots (warp-uniform)
+    uint64_t tn = (uint64_t)blockIdx.x * kSetWarps + warp;
+    const uint64_t tstride = (uint64_t)gridDim.x * kSetWarps;
+    for (;;) {
+        // ---- refill free slots: A2 + phase A of the next chunks ----
+        while (occ != (1u << kPark) - 1u && tn < P.p) {
+            const uint64_t t = tn;
+            tn += tstride;
+            const uint64_t b0 = conv_b(P, t), b1 = conv_b(P, t + 1);
+            // A2: R_t = L(T[b_t - 1]) (complete tables: S = Q), R_0 = {q0}
+            uint32_t D;
+            __syncwarp();
+            if (t == 0) {
+                bool dead;
+                D = 1;
+                if (lane == 0) list[0] = (uint16_t)start_state(P, &dead);
+            } else {
+                const uint32_t c = in[b0 - 1];
+                const uint32_t li = (P.cand == PAREM_CANDIDATES_ENUM || c >= d.A) ? d.A : c;
+                D = __ldg(d.Lcnt + li);
+                const uint32_t* L = d.Llist + __ldg(d.Loff + li);
+                for (uint32_t k = lane; k < D; k += 32) list[k] = (uint16_t)__ldg(L + k);
+            }
+            __syncwarp();
+            uint64_t pos = b0;
+            // phase A: more than 32 states -- the deduplicated image every step, compacted
+            // in place (a batch is read into registers before any of its writes land, and
+            // writes never pass the batch being read)
+            while (D > 32 && pos < b1) {
+                const uint32_t colc = T.col(__ldg(in + pos));
+                for (uint32_t i = lane; i < nbm; i += 32) bm[i] = 0u;
+                __syncwarp();
+                uint32_t nD = 0;
+                for (uint32_t base = 0; base < D; base += 128) {
+                    uint32_t ns[4];
+                    bool fresh[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t idx = base + 32u * j + lane;
+                        ns[j] = idx < D ? T.state(T.next(list[idx] * T.ES, colc)) : 0xFFFFFFFFu;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        fresh[j] = false;
+                        if (ns[j] != 0xFFFFFFFFu) {
+                            const uint32_t bit = 1u << (ns[j] & 31u);
+                            fresh[j] = !(atomicOr(bm + (ns[j] >> 5), bit) & bit);
+                        }
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, fresh[j]);
+                        if (fresh[j]) list[nD + __popc(bal & ltmask)] = (uint16_t)ns[j];
+                        nD += __popc(bal);
+                    }
+                    __syncwarp();
+                }
+                D = nD;
+                ++pos;
+            }
+            if (D > 32) {   // reached the chunk end in phase A
+                write_open(t, b0, b1);
+                continue;
+            }
+            const uint32_t e = (lane < D ? list[lane] : list[0]) * T.ES;
+            uint32_t leaders;
+            const uint32_t nd = distinct(e, leaders);
+            if (nd <= dmax) {
+                write_handover(t, pos - b0, e, leaders, nd);
+                continue;
+            }
+            if (pos >= b1) {
+                write_open(t, b0, b1);
+                continue;
+            }
+            const int k = __ffs(~occ) - 1;   // park it
+#pragma unroll
+            for (int j = 0; j < kPark; ++j)
+                if (j == k) {
+                    pt[j] = t;
+                    ppos[j] = pos;
+                    pb0[j] = b0;
+                    pb1[j] = b1;
+                    pe[j] = e;
+                }
+            occ |= 1u << k;
+        }
+        if (!occ) break;
+        // ---- phase B: advance every parked chunk by up to 32 bytes, chains interleaved ----
+        uint32_t cnt[kPark], mine[kPark], cmax = 0;
+#pragma unroll
+        for (int j = 0; j < kPark; ++j) {
+            cnt[j] = ((occ >> j) & 1u) ? (uint32_t)min((uint64_t)32, pb1[j] - ppos[j]) : 0u;
+            mine[j] = lane < cnt[j] ? (uint32_t)__ldg(in + ppos[j] + lane) : 0u;
+            cmax = max(cmax, cnt[j]);
+        }
+        for (uint32_t i = 0; i < cmax; ++i) {
+#pragma unroll
+            for (int j = 0; j < kPark; ++j) {
+                const uint32_t c = __shfl_sync(0xFFFFFFFFu, mine[j], i);
+                if (i < cnt[j]) pe[j] = T.next(pe[j], T.col(c));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kPark; ++j) {
+            if (!((occ >> j) & 1u)) continue;
+            ppos[j] += cnt[j];
+            uint32_t leaders;
+            const uint32_t nd = distinct(pe[j], leaders);
+            if (nd <= dmax) {
+                write_handover(pt[j], ppos[j] - pb0[j], pe[j], leaders, nd);
+                occ &= ~(1u << j);
+            } else if (ppos[j] >= pb1[j]) {
+                write_open(pt[j], pb0[j], pb1[j]);
+                occ &= ~(1u << j);
+            }
+        }
     }
 }
 
