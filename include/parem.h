@@ -187,6 +187,37 @@ const char* parem_last_error(void);
 /* Version string. */
 const char* parem_version(void);
 
+/* ---- regular-expression front end (host) ----
+ * Compiles a pattern of the paper's language (Table III): concatenation `ab`,
+ * Kleene star `a*`, union `a|b`, positive closure `a+`, range `[x..y]` (every alphabet
+ * byte with x <= byte <= y), optionality `a?`, groups `( )`; `\` quotes an operator byte.
+ * AST -> McNaughton-Yamada-Thompson NFA -> subset construction -> minimal DFA (Moore
+ * refinement), states numbered breadth-first from the start state (start = 0), complete
+ * table (an unmatched suffix leads to an explicit non-accepting trap state).
+ *   alphabet       NUL-terminated string of distinct bytes: symbol i is alphabet[i]; NULL or
+ *                  "" = the distinct bytes of the pattern in increasing order.  The input
+ *                  of a match is the symbol ids (mapping bytes to ids is the caller's job).
+ *   flags          PAREM_REGEX_SEARCH: compile Sigma* R, whose match count is the number
+ *                  of positions where an occurrence of R ends (the paper's "parallel"
+ *                  automaton, Table I); 0: the anchored language R.
+ *   max_states     capacity of `table` rows / `accept_bitmap` bits (0 = 65536).
+ *   table          host, row-major max_states x A uint32 (parem_dfa_create's layout), or
+ *                  NULL together with accept_bitmap for a size query (info only).
+ *   accept_bitmap  host, ceil(max_states / 8) bytes, LSB-first.
+ * Returns PAREM_OK, PAREM_EINVAL (syntax error / byte outside the alphabet / subset
+ * explosion; parem_last_error() names the offset) or PAREM_ENOMEM (max_states too small;
+ * info->num_states says how many are needed). */
+#define PAREM_REGEX_SEARCH 1u
+typedef struct parem_regex_info {
+    uint32_t num_states;
+    uint32_t alphabet_size;
+    uint32_t start_state;
+    uint32_t reserved;
+    char alphabet[256];   /* symbol i = alphabet[i] (alphabet_size bytes, not NUL-terminated) */
+} parem_regex_info;
+int parem_regex_compile(const char* pattern, const char* alphabet, uint32_t flags, uint32_t max_states,
+                        uint32_t* table, uint8_t* accept_bitmap, parem_regex_info* info);
+
 /* ---- per-kernel timing (bench.py; off by default) ----
  * parem_profile(1) clears the record and makes every later match issued by this host
  * thread record CUDA events on its stream around each kernel it launches (not while the

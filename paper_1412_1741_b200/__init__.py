@@ -21,7 +21,7 @@ from . import _abi
 from ._abi import (BOUNDARY_AUTO, BOUNDARY_GRID, BOUNDARY_SNAP, CANDIDATES_ENUM, CANDIDATES_PAREM, KERNEL_AUTO, KERNEL_CONV, KERNEL_LANES,
                    KERNEL_TINY, PAREM_DEAD, PAREM_EINVAL, PAREM_ESYMBOL, PAREM_OK)
 
-__all__ = ["Dfa", "MatchResult", "ParemError", "options", "profile", "profile_read", "PAREM_DEAD", "PAREM_OK",
+__all__ = ["Dfa", "MatchResult", "ParemError", "Regex", "compile_regex", "options", "profile", "profile_read", "PAREM_DEAD", "PAREM_OK",
            "PAREM_ESYMBOL", "PAREM_EINVAL", "lib"]
 
 
@@ -71,6 +71,44 @@ def options(chunk_len: int = 0, boundary: str = "auto", candidates: str = "parem
     o.kernel = _KERNEL[kernel]
     o.flags = _abi.FLAG_WS_CLEAN if ws_clean else 0
     return o
+
+
+class Regex(NamedTuple):
+    table: np.ndarray          # uint32 [num_states, alphabet_size], row-major (parem_dfa_create layout)
+    start: int
+    accept: np.ndarray         # bool [num_states]
+    alphabet: bytes            # symbol i = alphabet[i]
+
+    def encode(self, text: bytes) -> np.ndarray:
+        """Bytes -> symbol ids (raises on a byte outside the alphabet)."""
+        lut = np.full(256, 255, dtype=np.uint8)
+        lut[np.frombuffer(self.alphabet, dtype=np.uint8)] = np.arange(len(self.alphabet), dtype=np.uint8)
+        ids = lut[np.frombuffer(bytes(text), dtype=np.uint8)]
+        if len(self.alphabet) < 256 and (ids == 255).any():
+            raise ValueError("text has bytes outside the alphabet")
+        return ids
+
+
+def compile_regex(pattern: str | bytes, alphabet: str | bytes | None = None, search: bool = False,
+                  max_states: int = 1 << 16) -> Regex:
+    """parem_regex_compile: the paper's RE language (Table III) -> minimal DFA (NEXT-3).
+    ``search=True`` compiles Sigma* R (match count = occurrence end positions)."""
+    L = lib()
+    pat = pattern.encode("latin-1") if isinstance(pattern, str) else bytes(pattern)
+    alp = None if alphabet is None else (alphabet.encode("latin-1") if isinstance(alphabet, str) else bytes(alphabet))
+    info = _abi.parem_regex_info()
+    fl = _abi.REGEX_SEARCH if search else 0
+    st = L.parem_regex_compile(pat, alp, fl, 0, None, None, C.byref(info))
+    if st != PAREM_OK:
+        _err(L, st)
+    Q, A = info.num_states, info.alphabet_size
+    tab = np.zeros((Q, A), dtype=np.uint32)
+    bm = np.zeros((Q + 7) // 8, dtype=np.uint8)
+    st = L.parem_regex_compile(pat, alp, fl, Q, tab.ctypes.data, bm.ctypes.data, C.byref(info))
+    if st != PAREM_OK:
+        _err(L, st)
+    acc = np.unpackbits(bm, bitorder="little")[:Q].astype(bool)
+    return Regex(tab, int(info.start_state), acc, bytes(info.alphabet[:A]))
 
 
 def profile(enable: bool = True) -> None:

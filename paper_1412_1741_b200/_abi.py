@@ -32,6 +32,14 @@ class parem_kernel_time(C.Structure):
     _fields_ = [("name", C.c_char * 40), ("ms", C.c_float), ("match", C.c_uint32)]
 
 
+REGEX_SEARCH = 1
+
+
+class parem_regex_info(C.Structure):
+    _fields_ = [("num_states", C.c_uint32), ("alphabet_size", C.c_uint32), ("start_state", C.c_uint32),
+                ("reserved", C.c_uint32), ("alphabet", C.c_char * 256)]
+
+
 class parem_dfa_info(C.Structure):
     _fields_ = [("num_states", C.c_uint32), ("internal_states", C.c_uint32), ("alphabet_size", C.c_uint32),
                 ("has_sink", C.c_uint32), ("min_L", C.c_uint32), ("max_L", C.c_uint32), ("sum_L", C.c_uint64),
@@ -53,7 +61,7 @@ EXPORTS = [
     "parem_dfa_create", "parem_dfa_destroy", "parem_workspace_bytes", "parem_match_async",
     "parem_match_continue_async", "parem_match", "parem_match_host", "parem_dfa_get_info", "parem_plan",
     "parem_last_error", "parem_version", "parem_bench_read_stream", "parem_bench_gather", "parem_profile",
-    "parem_profile_read",
+    "parem_profile_read", "parem_regex_compile",
 ]
 
 _LIB = None
@@ -84,6 +92,8 @@ def load(path: str = SO_PATH):
     L.parem_match.argtypes = [vp, vp, u64, O, R, vp]
     L.parem_match_host.restype = i32
     L.parem_match_host.argtypes = [vp, vp, u64, O, R, vp]
+    L.parem_regex_compile.restype = i32
+    L.parem_regex_compile.argtypes = [C.c_char_p, C.c_char_p, u32, u32, vp, vp, C.POINTER(parem_regex_info)]
     L.parem_profile.restype = i32
     L.parem_profile.argtypes = [i32]
     L.parem_profile_read.restype = i32

@@ -19,6 +19,15 @@ __device__ __forceinline__ uint4 ldg_v4(const uint8_t* p) {
     return v;
 }
 
+// streaming input: do not allocate in L1 (keeps L1 for L2-resident transition tables)
+__device__ __forceinline__ uint4 ldg_v4_na(const uint8_t* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ unsigned long long ld_cg_u64(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));

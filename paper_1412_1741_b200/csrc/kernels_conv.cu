@@ -297,10 +297,10 @@ __device__ __forceinline__ uint32_t follow_vecs(const Tab<SMEM, W32>& T, const u
                                                 uint32_t nvmax, uint32_t A, uint32_t* e, uint32_t* h, uint32_t& bad) {
     // the next 16 bytes are loaded while the current ones are walked (one vector in flight
     // per thread hides the HBM latency behind the dependent lookups)
-    uint4 nx = v < nv ? ldg_v4(p + 16ull * v) : make_uint4(0, 0, 0, 0);
+    uint4 nx = v < nv ? ldg_v4_na(p + 16ull * v) : make_uint4(0, 0, 0, 0);
     for (; v < nvmax; ++v) {
         const uint4 x = nx;
-        if (v + 1 < nv) nx = ldg_v4(p + 16ull * (v + 1));
+        if (v + 1 < nv) nx = ldg_v4_na(p + 16ull * (v + 1));
         if (v < nv) {
             bad |= badbits(x.x, A) | badbits(x.y, A) | badbits(x.z, A) | badbits(x.w, A);
             const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
@@ -422,10 +422,10 @@ __device__ __forceinline__ uint32_t walk1(const DevDfa& d, const uint8_t* in, ui
         e = T.next(e, T.col(in[a]));
         h += T.hit(e);
     }
-    uint4 nx = a + 16 <= b ? ldg_v4(in + a) : make_uint4(0, 0, 0, 0);
+    uint4 nx = a + 16 <= b ? ldg_v4_na(in + a) : make_uint4(0, 0, 0, 0);
     for (; a + 16 <= b; a += 16) {
         const uint4 x = nx;
-        if (a + 32 <= b) nx = ldg_v4(in + a + 16);
+        if (a + 32 <= b) nx = ldg_v4_na(in + a + 16);
         const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
         for (int q2 = 0; q2 < 4; ++q2)
@@ -595,6 +595,12 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(conv_set_kernel<SMEM, W32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(conv_follow_kernel<SMEM, W32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb);
+    if (!SMEM && e == cudaSuccess) {
+        // global (L2-resident) tables: give the unified L1/shared array to L1
+        cudaFuncSetAttribute(conv_follow_kernel<SMEM, W32>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+        cudaFuncSetAttribute(conv_heads_kernel<W32>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+        cudaFuncSetAttribute(conv_join_kernel<W32>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    }
     if (e != cudaSuccess) {
         set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
         return PAREM_ECUDA;
