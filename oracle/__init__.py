@@ -52,6 +52,8 @@ def lib():
         L.oracle_walk.argtypes = [u32, u32, p, u32, u32, p, p, u64, C.POINTER(_Res)]
         L.oracle_states_at.restype = C.c_int
         L.oracle_states_at.argtypes = [u32, u32, p, u32, u32, p, u64, p, u64, p]
+        L.oracle_positions.restype = C.c_int
+        L.oracle_positions.argtypes = [u32, u32, p, u32, u32, p, p, u64, p, u64, C.POINTER(u64)]
         L.oracle_route_stats.restype = C.c_int
         L.oracle_route_stats.argtypes = [u32, u32, p, u32, p, u64, p, u64,
                                          C.POINTER(u64), C.POINTER(u64), p]
@@ -91,6 +93,22 @@ def walk(table, start: int, accept, text) -> Result:
     lib().oracle_walk(Q, A, t.ctypes.data, t.itemsize, start, bm.ctypes.data,
                       T.ctypes.data if T.size else None, T.size, C.byref(r))
     return Result(r.final_state, bool(r.accepted), r.match_count, r.status, r.bad_offset)
+
+
+def positions(table, start: int, accept, text, cap: int | None = None) -> tuple[np.ndarray, int]:
+    """Match end offsets (every k with q_{k+1} in F, ascending) and their total count."""
+    t = _tab(table)
+    Q, A = t.shape
+    T = _bytes(text)
+    bm = _bitmap(accept, Q)
+    cap = T.size if cap is None else cap
+    out = np.empty(max(1, cap), dtype=np.uint64)
+    cnt = C.c_uint64()
+    rc = lib().oracle_positions(Q, A, t.ctypes.data, t.itemsize, start, bm.ctypes.data,
+                                T.ctypes.data if T.size else None, T.size, out.ctypes.data, cap, C.byref(cnt))
+    if rc != OK:
+        raise ValueError(f"oracle_positions failed ({rc})")
+    return out[: min(cap, cnt.value)], int(cnt.value)
 
 
 def states_at(table, start: int, text, offsets) -> np.ndarray:

@@ -81,6 +81,34 @@ int oracle_walk(uint32_t Q, uint32_t A, const void* table, uint32_t eb, uint32_t
     return ORACLE_OK;
 }
 
+/* Match end positions (NEXT-4; Alg. 1's visited-state vector Rr, reduced to the
+ * steps whose destination is in F): every k in [0, n) with q_{k+1} in F, ascending, i.e.
+ * the 0-based offset of the symbol that completes an occurrence.  Writes min(count, cap)
+ * offsets; *count = all of them (= oracle_walk's match_count).  Stops at DEAD (C9);
+ * ESYMBOL as oracle_walk (C11). */
+int oracle_positions(uint32_t Q, uint32_t A, const void* table, uint32_t eb, uint32_t q0,
+                     const uint8_t* acc_bitmap, const uint8_t* T, uint64_t n, uint64_t* pos, uint64_t cap,
+                     uint64_t* count) {
+    *count = 0;
+    if (Q == 0 || A == 0 || A > 256 || q0 >= Q || (eb != 2 && eb != 4)) return ORACLE_EINVAL;
+    for (uint64_t k = 0; k < n; ++k)
+        if (T[k] >= A) return ORACLE_ESYMBOL;
+    uint32_t s = q0;
+    uint64_t c = 0;
+    for (uint64_t k = 0; k < n; ++k) {
+        uint32_t e = delta(table, eb, A, s, T[k]);
+        if (e == ORACLE_DEAD) break;
+        if (e >= Q) return ORACLE_EINVAL;
+        s = e;
+        if (in_F(acc_bitmap, s)) {
+            if (c < cap) pos[c] = k;
+            ++c;
+        }
+    }
+    *count = c;
+    return ORACLE_OK;
+}
+
 /* State after consuming T[0..offsets[j]) for ascending offsets (ORACLE_DEAD once dead).
  * Used for the speculation-soundness checks: the true boundary state lies in R_i. */
 int oracle_states_at(uint32_t Q, uint32_t A, const void* table, uint32_t eb, uint32_t q0,

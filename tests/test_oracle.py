@@ -169,3 +169,41 @@ def test_invalid_arguments():
     assert r.status == oracle.EINVAL
     r = oracle.walk(np.array([[0]], dtype=np.uint16), 3, np.array([False]), [0])
     assert r.status == oracle.EINVAL
+
+
+# ---------------------------------------------------------------- NEXT-4: match positions
+def test_positions_kmp_against_substring_search():
+    """Match end offsets of the Sigma*P automaton = j + |P| - 1 for every (overlapping)
+    occurrence P = T[j : j + |P|], found by naive substring search."""
+    rng = np.random.default_rng(11)
+    for P in ([0, 1, 2, 1, 4, 4, 3, 4], [0, 0, 1], [2, 2, 2]):
+        t = synth.kmp_dfa(P, 5, np.uint16)
+        acc = np.zeros(len(P) + 1, dtype=bool)
+        acc[-1] = True
+        x = rng.integers(0, 5, 20000).astype(np.uint8)
+        for pos in rng.integers(0, 20000 - len(P), 40):
+            x[pos:pos + len(P)] = P
+        want = [j + len(P) - 1 for j in range(x.size - len(P) + 1) if list(x[j:j + len(P)]) == list(P)]
+        got, cnt = oracle.positions(t, 0, acc, x)
+        assert got.tolist() == want and cnt == len(want) == oracle.walk(t, 0, acc, x).match_count
+
+
+def test_positions_abb_regex_and_caps():
+    """(a|b)*abb: offsets k with re.fullmatch on the prefix T[:k+1]; a cap keeps the first
+    offsets and still reports the full count; DEAD stops the list (C9)."""
+    t = np.array([[1, 0], [1, 2], [1, 3], [1, 0]], dtype=np.uint32)
+    acc = np.array([False, False, False, True])
+    rng = np.random.default_rng(3)
+    x = rng.integers(0, 2, 3000).astype(np.uint8)
+    s = "".join("ab"[c] for c in x)
+    want = [k for k in range(len(s)) if re.fullmatch("(a|b)*abb", s[: k + 1])]
+    got, cnt = oracle.positions(t, 0, acc, x)
+    assert got.tolist() == want and cnt == len(want)
+    got5, cnt5 = oracle.positions(t, 0, acc, x, cap=5)
+    assert got5.tolist() == want[:5] and cnt5 == len(want)
+    tp = np.array([[1, 0], [0xFFFF, 3], [1, 3], [3, 3]], dtype=np.uint16)
+    accp = np.array([False, True, False, True])
+    got, cnt = oracle.positions(tp, 0, accp, np.array([0, 1, 0, 0, 1], np.uint8))   # 0 -a-> 1 -b-> 3 -> 3 -> 3
+    assert got.tolist() == [0, 1, 2, 3, 4] and cnt == 5
+    got, cnt = oracle.positions(tp, 0, accp, np.array([0, 0, 1], np.uint8))   # dies at offset 1
+    assert got.tolist() == [0] and cnt == 1
