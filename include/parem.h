@@ -187,6 +187,20 @@ const char* parem_last_error(void);
 /* Version string. */
 const char* parem_version(void);
 
+/* ---- match positions (Alg. 1's visited states Rr) ----
+ * parem_find_async runs the match of parem_match_async (same d_result) and then writes the
+ * offsets k, ascending, of every step whose state is in F (k = 0-based offset of the symbol
+ * that completes an occurrence; their number is d_result->match_count) to d_positions
+ * (device, caller-owned, max_positions u64 entries; only the first max_positions are
+ * written).  Every chunk's true entering state is resolved from the composition, the hit
+ * counts are exclusive-scanned into output offsets and each chunk is walked once more from
+ * its true state.  Workspace: parem_find_workspace_bytes (>= parem_workspace_bytes).  On an
+ * ESYMBOL result the positions are unspecified.  n = 0 writes nothing. */
+size_t parem_find_workspace_bytes(const parem_dfa* dfa, uint64_t n, const parem_options* opts);
+int parem_find_async(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, void* d_ws, size_t ws_bytes,
+                     const parem_options* opts, uint64_t* d_positions, uint64_t max_positions,
+                     parem_result* d_result, void* stream);
+
 /* ---- regular-expression front end (host) ----
  * Compiles a pattern of the paper's language (Table III): concatenation `ab`,
  * Kleene star `a*`, union `a|b`, positive closure `a+`, range `[x..y]` (every alphabet

@@ -242,6 +242,37 @@ class Dfa:
         if st != PAREM_OK:
             _err(self._L, st)
 
+    def find_workspace_bytes(self, n: int, opts=None) -> int:
+        ws = self._L.parem_find_workspace_bytes(self._h, n, C.byref(opts) if opts is not None else None)
+        if ws == 0:
+            _err(self._L, PAREM_EINVAL)
+        return ws
+
+    def find_async(self, x, ws, positions, result, opts=None, stream=None) -> None:
+        """Enqueue parem_find_async: the match plus its match END offsets (uint64, ascending)
+        into the CUDA tensor ``positions`` (at most positions.numel() are written)."""
+        x = _cuda_u8(x)
+        st = self._L.parem_find_async(self._h, C.c_void_p(x.data_ptr()), x.numel(), C.c_void_p(ws.data_ptr()),
+                                      ws.numel(), C.byref(opts) if opts is not None else None,
+                                      C.c_void_p(positions.data_ptr()) if positions.numel() else None,
+                                      positions.numel(), C.c_void_p(result.data_ptr()), _stream(stream))
+        if st != PAREM_OK:
+            _err(self._L, st)
+
+    def find(self, x, max_positions: int | None = None, opts=None):
+        """Synchronous find: (MatchResult, positions as a CUDA int64 tensor of
+        min(match_count, max_positions) offsets).  max_positions=None sizes for every byte."""
+        import torch
+
+        x = _cuda_u8(x)
+        cap = x.numel() if max_positions is None else int(max_positions)
+        ws = torch.zeros(self.find_workspace_bytes(x.numel(), opts), dtype=torch.uint8, device=x.device)
+        pos = torch.empty(max(cap, 1), dtype=torch.int64, device=x.device)
+        res = torch.zeros(64, dtype=torch.uint8, device=x.device)
+        self.find_async(x, ws, pos[:cap], res, opts)
+        r = MatchResult.from_bytes(res.cpu().numpy().tobytes()[:56])
+        return r, pos[: min(cap, r.match_count)]
+
     def match_continue_async(self, x, offset_base: int, ws, carry, result, opts=None, stream=None) -> None:
         x = _cuda_u8(x)
         st = self._L.parem_match_continue_async(

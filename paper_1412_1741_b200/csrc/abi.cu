@@ -86,7 +86,8 @@ void prof_after(const char* name, cudaStream_t s) {
 
 static int match_impl(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, uint64_t offset_base, void* d_ws,
                       size_t ws_bytes, const parem_options* opts, const parem_result* d_carry,
-                      parem_result* d_result, cudaStream_t stream) {
+                      parem_result* d_result, cudaStream_t stream, uint64_t* d_positions = nullptr,
+                      uint64_t max_positions = 0, bool find = false) {
     set_error("");
     if (!dfa || !d_result) { set_error("null dfa or result"); return PAREM_EINVAL; }
     if (n > 0 && !d_input) { set_error("null input"); return PAREM_EINVAL; }
@@ -95,9 +96,14 @@ static int match_impl(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, 
     if (rc != PAREM_OK) return rc;
     if (!d_ws || (reinterpret_cast<uintptr_t>(d_ws) & 15)) { set_error("null or unaligned (16 B) workspace"); return PAREM_EINVAL; }
     if (d_result && (reinterpret_cast<uintptr_t>(d_result) & 7)) { set_error("result must be 8-byte aligned"); return PAREM_EINVAL; }
-    if (ws_bytes < plan.ws) {
-        set_error("workspace too small: %zu < %zu", ws_bytes, plan.ws);
+    const size_t need = find ? ((plan.ws + 255) & ~(size_t)255) + find_extra_bytes(plan, dfa->dev) : plan.ws;
+    if (ws_bytes < need) {
+        set_error("workspace too small: %zu < %zu", ws_bytes, need);
         return PAREM_ENOMEM;
+    }
+    if (find && max_positions && !d_positions) {
+        set_error("null positions buffer");
+        return PAREM_EINVAL;
     }
     MatchParams P;
     memset(&P, 0, sizeof(P));
@@ -127,9 +133,18 @@ static int match_impl(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, 
     }
     prof_begin(stream);
     if (plan.kernel == kKernelTrivial) return launch_trivial(P, stream);
-    if (plan.kernel == kKernelTiny) return launch_tiny(plan, P, stream);
-    if (plan.kernel == kKernelConv) return launch_conv(plan, P, stream);
-    return launch_lanes(plan, P, stream);
+    if (find) {
+        find_bind(plan, P, reinterpret_cast<unsigned char*>(d_ws) + ((plan.ws + 255) & ~(size_t)255));
+        P.fout = d_positions;
+        P.fmax = d_positions ? max_positions : 0;
+        if (plan.kernel != kKernelTiny) P.fmend = nullptr;   // only the tiny kernel keeps dense maps
+    }
+    int rc2;
+    if (plan.kernel == kKernelTiny) rc2 = launch_tiny(plan, P, stream);
+    else if (plan.kernel == kKernelConv) rc2 = launch_conv(plan, P, stream);
+    else rc2 = launch_lanes(plan, P, stream);
+    if (rc2 != PAREM_OK || !find) return rc2;
+    return launch_find(plan, P, stream);
 }
 
 }  // namespace parem
@@ -324,6 +339,20 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint16_t* __restrict_
 }
 
 }  // namespace parem
+
+extern "C" size_t parem_find_workspace_bytes(const parem_dfa* dfa, uint64_t n, const parem_options* opts) {
+    Plan plan;
+    if (make_plan(dfa, n, opts, &plan) != PAREM_OK) return 0;
+    if (plan.kernel == kKernelTrivial) return plan.ws;
+    return ((plan.ws + 255) & ~(size_t)255) + find_extra_bytes(plan, dfa->dev);
+}
+
+extern "C" int parem_find_async(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, void* d_ws, size_t ws_bytes,
+                                const parem_options* opts, uint64_t* d_positions, uint64_t max_positions,
+                                parem_result* d_result, void* stream) {
+    return match_impl(dfa, d_input, n, 0, d_ws, ws_bytes, opts, nullptr, d_result, (cudaStream_t)stream, d_positions,
+                      max_positions, true);
+}
 
 extern "C" int parem_profile(int enable) {
     ProfState& p = g_prof;

@@ -73,6 +73,18 @@ struct MatchParams {
     WsHeader* hdr;
     void* maps;                // tiny: tile maps [grid][Qpad] u64; lanes: ends [p][Qpad] u32 + hits
     uint32_t* map_hits;        // lanes only
+    // parem_find_async (NEXT-4; kernels_find.cu): null for a plain match
+    uint64_t* fout;            // match end offsets
+    uint64_t fmax;             // capacity of fout
+    uint32_t* fchunk_q;        // [p] entering state of chunk i
+    uint32_t* fchunk_h;        // [p] hits of chunk i from that state
+    unsigned long long* fchunk_base;   // [p] exclusive prefix of fchunk_h
+    unsigned long long* fblock;        // scan block sums
+    uint32_t* fgq;             // tiny: entering state per group of 32 chunks
+    uint8_t* fmend;            // tiny: per-chunk dense maps (end) [p][Qpad]
+    uint32_t* fmhits;          // tiny: per-chunk dense maps (hits) [p][Qpad]
+    uint32_t* fgend;           // tiny: per-group maps (end) [groups][Qpad]
+    unsigned long long* fghits;        // tiny: per-group maps (hits)
 };
 
 struct Plan {
@@ -119,6 +131,9 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
 int launch_tiny(const Plan& plan, const MatchParams& P, cudaStream_t s);
 int launch_lanes(const Plan& plan, const MatchParams& P, cudaStream_t s);
 int launch_conv(const Plan& plan, const MatchParams& P, cudaStream_t s);
+int launch_find(const Plan& plan, const MatchParams& P, cudaStream_t s);
+size_t find_extra_bytes(const Plan& plan, const DevDfa& d);
+void find_bind(const Plan& plan, MatchParams& P, unsigned char* extra);
 size_t conv_chunk_bytes();
 size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap);
 int launch_trivial(const MatchParams& P, cudaStream_t s);

@@ -542,6 +542,10 @@ __global__ void __launch_bounds__(kFollowThreads) conv_heads_kernel(const MatchP
             }
         }
         if (t == P.p - 1) P.hdr->final_q = fin;
+        if (P.fchunk_q) {   // parem_find_async: entering state and hits of this chunk
+            P.fchunk_q[t] = c.q;
+            P.fchunk_h[t] = (uint32_t)hits;
+        }
         const uint64_t off = first_bad(P.in, b0, b0 + c.m, d.A);
         if (off < b0 + c.m) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
         // stats: |R_t| (R_0 = {q0}) and |R_t| * len_t

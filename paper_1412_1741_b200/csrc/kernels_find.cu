@@ -1,0 +1,293 @@
+// kernels_find.cu -- SURVEY §8(f) NEXT-4: match END positions.  Alg. 1 keeps a visited-state
+// vector Rr per route; the positions of the matches are the steps whose state is
+// in F.  After a match has produced its per-chunk maps (tiny / lanes kernels) or the true
+// boundary states (converging path), every chunk's entering state q_i and hit count h_i are
+// resolved, h is exclusive-scanned into output offsets, and every chunk is walked ONCE more
+// from q_i -- one route per chunk, no speculation -- writing the offsets k (q_{k+1} in F) of
+// its matches to out[base_i + j] (ascending overall; at most max_positions are written).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels_common.cuh"
+
+namespace parem {
+
+namespace {
+
+constexpr uint32_t kFindThreads = 256;
+constexpr uint32_t kScanBlock = 1024;   // chunks per scan block (one CTA, 4 per thread)
+constexpr uint32_t kGroup = 32;         // tiny path: chunks per composed group
+
+// chunk boundaries exactly as the match computed them
+__device__ __forceinline__ uint64_t find_b(const MatchParams& P, uint64_t i) {
+    return boundary_of(P, i, P.d.Lcnt);
+}
+
+// ---- tiny path: compose groups of 32 chunk maps (lane q = start state q) ----
+__global__ void __launch_bounds__(kFindThreads) find_group_kernel(const MatchParams P, uint64_t groups) {
+    const uint64_t g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31u, Qpad = P.d.Qpad;
+    if (g >= groups) return;
+    uint32_t ce = lane < Qpad ? lane : 0;
+    unsigned long long ch = 0;
+    const uint64_t lo = g * kGroup, hi = min(P.p, lo + kGroup);
+    for (uint64_t i = lo; i < hi; ++i) {
+        const uint64_t r = i * Qpad + ce;
+        ch += P.fmhits[r];
+        ce = P.fmend[r];
+    }
+    if (lane < Qpad) {
+        P.fgend[g * Qpad + lane] = ce;
+        P.fghits[g * Qpad + lane] = ch;
+    }
+}
+
+// ---- tiny path: one warp walks the group maps along q0's path (shuffles, lane = state);
+// the maps of 32 groups are loaded at once so the loads overlap ----
+__global__ void find_group_seq_kernel(const MatchParams P, uint64_t groups) {
+    const uint32_t lane = threadIdx.x & 31u, Qpad = P.d.Qpad;
+    if (threadIdx.x >= 32) return;
+    bool dead;
+    uint32_t q = start_state(P, &dead);
+    for (uint64_t g0 = 0; g0 < groups; g0 += 32) {
+        uint32_t e[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            e[j] = (g0 + j < groups && lane < Qpad) ? P.fgend[(g0 + j) * Qpad + lane] : 0u;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (g0 + j < groups) {
+                if (lane == 0) P.fgq[g0 + j] = q;   // entering state of group g0 + j
+                q = __shfl_sync(0xFFFFFFFFu, e[j], q);
+            }
+        }
+    }
+}
+
+// ---- tiny path: per chunk q_i and h_i, one thread per group walking its 32 chunk maps ----
+__global__ void __launch_bounds__(kFindThreads) find_chunks_kernel(const MatchParams P, uint64_t groups) {
+    const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= groups) return;
+    const uint32_t Qpad = P.d.Qpad;
+    uint32_t q = P.fgq[g];
+    const uint64_t lo = g * kGroup, hi = min(P.p, lo + kGroup);
+    for (uint64_t i = lo; i < hi; ++i) {
+        const uint64_t r = i * Qpad + q;
+        P.fchunk_q[i] = q;
+        P.fchunk_h[i] = P.fmhits[r];
+        q = P.fmend[r];
+    }
+}
+
+// ---- lanes path: one thread walks the p dense chunk maps (p is small on this path) ----
+__global__ void find_lanes_seq_kernel(const MatchParams P) {
+    if (threadIdx.x != 0) return;
+    const uint32_t* mend = reinterpret_cast<const uint32_t*>(P.maps);
+    bool dead;
+    uint32_t q = start_state(P, &dead);
+    for (uint64_t i = 0; i < P.p; ++i) {
+        P.fchunk_q[i] = q;
+        if (P.d.has_sink && q == P.d.sink) {   // dead: absorbing, no hits (C9); map rows of the
+            P.fchunk_h[i] = 0;                 // sink are not written by the lanes kernel
+            continue;
+        }
+        const uint64_t r = i * P.d.Qpad + q;
+        P.fchunk_h[i] = P.map_hits[r];
+        q = mend[r];
+    }
+}
+
+// ---- exclusive scan of the per-chunk hit counts (u32) into u64 output offsets ----
+__global__ void __launch_bounds__(kScanBlock / 4) find_scan_sums_kernel(const MatchParams P) {
+    __shared__ unsigned long long ws[kScanBlock / 4 / 32];
+    const uint64_t base = (uint64_t)blockIdx.x * kScanBlock;
+    unsigned long long s = 0;
+    for (uint32_t k = 0; k < 4; ++k) {
+        const uint64_t i = base + threadIdx.x * 4 + k;
+        if (i < P.p) s += P.fchunk_h[i];
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31u) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (uint32_t w = 0; w < kScanBlock / 4 / 32; ++w) t += ws[w];
+        P.fblock[blockIdx.x] = t;
+    }
+}
+
+__global__ void find_scan_blocks_kernel(const MatchParams P, uint64_t nblocks) {
+    if (threadIdx.x != 0) return;
+    unsigned long long run = 0;
+    for (uint64_t b = 0; b < nblocks; ++b) {
+        const unsigned long long v = P.fblock[b];
+        P.fblock[b] = run;
+        run += v;
+    }
+}
+
+__global__ void __launch_bounds__(kScanBlock / 4) find_scan_apply_kernel(const MatchParams P) {
+    __shared__ unsigned long long ws[kScanBlock / 4 / 32];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint64_t base = (uint64_t)blockIdx.x * kScanBlock;
+    uint32_t v[4];
+    unsigned long long s = 0;
+    for (uint32_t k = 0; k < 4; ++k) {
+        const uint64_t i = base + threadIdx.x * 4 + k;
+        v[k] = i < P.p ? P.fchunk_h[i] : 0u;
+        s += v[k];
+    }
+    // inclusive warp scan of the per-thread sums
+    unsigned long long inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if ((int)lane >= o) inc += y;
+    }
+    if (lane == 31) ws[warp] = inc;
+    __syncthreads();
+    unsigned long long woff = 0;
+    for (uint32_t w = 0; w < warp; ++w) woff += ws[w];
+    unsigned long long run = P.fblock[blockIdx.x] + woff + inc - s;
+    for (uint32_t k = 0; k < 4; ++k) {
+        const uint64_t i = base + threadIdx.x * 4 + k;
+        if (i < P.p) P.fchunk_base[i] = run;
+        run += v[k];
+    }
+}
+
+// ---- emit: walk every chunk once from its true entering state ----
+// tiny tables: tab1[s][c] = dest | acc(dest) << 15 (u16), staged in shared memory
+__global__ void __launch_bounds__(kFindThreads) find_emit_tiny_kernel(const MatchParams P) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const DevDfa& d = P.d;
+    uint16_t* tab = reinterpret_cast<uint16_t*>(sm);
+    for (uint32_t i = threadIdx.x; i < d.Qp * d.A; i += blockDim.x) tab[i] = __ldg(d.tab1 + i);
+    __syncthreads();
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= P.p) return;
+    const uint64_t b0 = find_b(P, t), b1 = find_b(P, t + 1);
+    uint32_t s = P.fchunk_q[t];
+    unsigned long long o = P.fchunk_base[t];
+    const uint32_t A = d.A;
+    auto step = [&](uint32_t c, uint64_t k) {
+        const uint32_t e = tab[s * A + (c < A ? c : A - 1)];
+        s = e & 0x7FFFu;
+        if (e >> 15) {
+            if (o < P.fmax) P.fout[o] = k;
+            ++o;
+        }
+    };
+    uint64_t a = b0;
+    for (; a < b1 && (((uintptr_t)(P.in + a)) & 15u); ++a) step(P.in[a], a);
+    for (; a + 16 <= b1; a += 16) {
+        const uint4 x = ldg_v4_na(P.in + a);
+        const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k) step(__byte_perm(w4[q], 0u, 0x4440u | k), a + 4 * q + k);
+    }
+    for (; a < b1; ++a) step(P.in[a], a);
+}
+
+// symbol-major lanes tables (entry = dest * ES | acc << (8 ES - 1)), global / L2
+template <bool W32>
+__global__ void __launch_bounds__(kFindThreads) find_emit_lanes_kernel(const MatchParams P) {
+    const DevDfa& d = P.d;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= P.p) return;
+    constexpr uint32_t ES = W32 ? 4 : 2, ACC = W32 ? 31 : 15;
+    const uint32_t COL = d.Qpad * ES, SMASK = (d.Qpad - 1u) * ES, CMASK = d.Apad - 1u;
+    const unsigned char* g = reinterpret_cast<const unsigned char*>(d.lanes_tab);
+    const uint64_t b0 = find_b(P, t), b1 = find_b(P, t + 1);
+    uint32_t e = P.fchunk_q[t] * ES;
+    unsigned long long o = P.fchunk_base[t];
+    auto step = [&](uint32_t c, uint64_t k) {
+        const uint32_t off = (e & SMASK) | ((c & CMASK) * COL);
+        e = W32 ? __ldg(reinterpret_cast<const uint32_t*>(g + off)) : __ldg(reinterpret_cast<const uint16_t*>(g + off));
+        if (e >> ACC) {
+            if (o < P.fmax) P.fout[o] = k;
+            ++o;
+        }
+    };
+    uint64_t a = b0;
+    for (; a < b1 && (((uintptr_t)(P.in + a)) & 15u); ++a) step(P.in[a], a);
+    for (; a + 16 <= b1; a += 16) {
+        const uint4 x = ldg_v4_na(P.in + a);
+        const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k) step(__byte_perm(w4[q], 0u, 0x4440u | k), a + 4 * q + k);
+    }
+    for (; a < b1; ++a) step(P.in[a], a);
+}
+
+unsigned nblk(uint64_t n, uint32_t per) { return (unsigned)((n + per - 1) / per); }
+
+}  // namespace
+
+// Workspace after the match's own: q, h per chunk; u64 bases; scan block sums; tiny path:
+// per-chunk maps (end u8, hits u32) and per-group maps.
+size_t find_extra_bytes(const Plan& plan, const DevDfa& d) {
+    const uint64_t p = plan.p, groups = (p + kGroup - 1) / kGroup, nb = (p + kScanBlock - 1) / kScanBlock;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    size_t s = al(4 * p) + al(4 * p) + al(8 * p) + al(8 * nb) + al(4 * groups);
+    if (plan.kernel == kKernelTiny)
+        s += al((size_t)p * d.Qpad) + al(4 * (size_t)p * d.Qpad) + al(4 * (size_t)groups * d.Qpad) +
+             al(8 * (size_t)groups * d.Qpad);
+    return s;
+}
+
+void find_bind(const Plan& plan, MatchParams& P, unsigned char* extra) {
+    const uint64_t p = plan.p, groups = (p + kGroup - 1) / kGroup, nb = (p + kScanBlock - 1) / kScanBlock;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    unsigned char* o = extra;
+    P.fchunk_q = reinterpret_cast<uint32_t*>(o); o += al(4 * p);
+    P.fchunk_h = reinterpret_cast<uint32_t*>(o); o += al(4 * p);
+    P.fchunk_base = reinterpret_cast<unsigned long long*>(o); o += al(8 * p);
+    P.fblock = reinterpret_cast<unsigned long long*>(o); o += al(8 * nb);
+    P.fgq = reinterpret_cast<uint32_t*>(o); o += al(4 * groups);
+    if (plan.kernel == kKernelTiny) {
+        P.fmend = o; o += al((size_t)p * P.d.Qpad);
+        P.fmhits = reinterpret_cast<uint32_t*>(o); o += al(4 * (size_t)p * P.d.Qpad);
+        P.fgend = reinterpret_cast<uint32_t*>(o); o += al(4 * (size_t)groups * P.d.Qpad);
+        P.fghits = reinterpret_cast<unsigned long long*>(o); o += al(8 * (size_t)groups * P.d.Qpad);
+    }
+}
+
+int launch_find(const Plan& plan, const MatchParams& P, cudaStream_t s) {
+    const uint64_t p = plan.p, groups = (p + kGroup - 1) / kGroup, nb = (p + kScanBlock - 1) / kScanBlock;
+    if (plan.kernel == kKernelTiny) {
+        find_group_kernel<<<nblk(groups * 32, kFindThreads), kFindThreads, 0, s>>>(P, groups);
+        prof_after("find_group", s);
+        find_group_seq_kernel<<<1, 32, 0, s>>>(P, groups);
+        find_chunks_kernel<<<nblk(groups, kFindThreads), kFindThreads, 0, s>>>(P, groups);
+        prof_after("find_resolve", s);
+    } else if (plan.kernel == kKernelLanes) {
+        find_lanes_seq_kernel<<<1, 32, 0, s>>>(P);
+        prof_after("find_resolve", s);
+    }   // converging path: q_i and h_i were written by conv_heads
+    find_scan_sums_kernel<<<(unsigned)nb, kScanBlock / 4, 0, s>>>(P);
+    find_scan_blocks_kernel<<<1, 32, 0, s>>>(P, nb);
+    find_scan_apply_kernel<<<(unsigned)nb, kScanBlock / 4, 0, s>>>(P);
+    prof_after("find_scan", s);
+    if (plan.kernel == kKernelTiny) {
+        const size_t smem = (size_t)P.d.Qp * P.d.A * 2;
+        find_emit_tiny_kernel<<<nblk(p, kFindThreads), kFindThreads, smem, s>>>(P);
+    } else if (P.d.lanes_u32) {
+        find_emit_lanes_kernel<true><<<nblk(p, kFindThreads), kFindThreads, 0, s>>>(P);
+    } else {
+        find_emit_lanes_kernel<false><<<nblk(p, kFindThreads), kFindThreads, 0, s>>>(P);
+    }
+    prof_after("find_emit", s);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("find kernels: %s", cudaGetErrorString(e));
+        return PAREM_ECUDA;
+    }
+    return PAREM_OK;
+}
+
+}  // namespace parem

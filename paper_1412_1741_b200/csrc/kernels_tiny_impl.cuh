@@ -442,6 +442,12 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
                     mhits[lr * Qpad + s] = x.h[j];
                 }
         }
+        if (P.fmend) {   // parem_find_async: keep this chunk's dense map for the position pass
+            for (uint32_t q = 0; q < Qpad; ++q) {
+                P.fmend[c.t * Qpad + q] = mend[lr * Qpad + q];
+                P.fmhits[c.t * Qpad + q] = mhits[lr * Qpad + q];
+            }
+        }
         if (c.cnt == 0 && first_bad(P.in, c.b0, c.b1, A) < c.b1) badacc = 1;   // R_i empty: still validate
         if (badacc) {
             const uint64_t off = first_bad(P.in, c.b0, c.b1, A);

@@ -390,3 +390,56 @@ def test_profile_records_kernels(parem, torch_mod):
     names = [r[1] for r in recs]
     assert names == ["conv_set", "conv_follow", "conv_join", "conv_join_seq", "conv_heads"] * 2
     assert {r[0] for r in recs} == {0, 1} and all(r[2] > 0 for r in recs)
+
+
+# ---------------------------------------------------------------- NEXT-4: match positions
+def check_find(parem, torch, table, start, acc, x, opts=None, cap=None, offset=0):
+    pos_ref, cnt_ref = oracle.positions(table, start, acc, x, cap=cap)
+    with parem.Dfa(table, start, acc) as d:
+        r, pos = d.find(to_dev(torch, x, offset), max_positions=cap, opts=opts)
+    assert r.status == 0 and r.match_count == cnt_ref, (r, cnt_ref)
+    got = pos.cpu().numpy().astype(np.uint64)
+    assert got.size == pos_ref.size and (got == pos_ref).all(), (got[:10], pos_ref[:10])
+    return r
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_find_configs(parem, torch_mod, k):
+    """Match end offsets on every BASELINE config (CI size, ragged tail): tiny, converging
+    path; ascending, element by element against the oracle."""
+    c = synth.config(k, n=(1 << 20) + 333)
+    x = c.make_input()
+    check_find(parem, torch_mod, c.table, c.start, c.accept, x)
+
+
+@pytest.mark.parametrize("kernel,L,cand,boundary", [("auto", 0, "parem", "auto"), ("auto", 1000, "parem", "snap"),
+                                                    ("auto", 64, "enum", "grid"), ("lanes", 0, "parem", "snap"),
+                                                    ("lanes", 5000, "enum", "grid"), ("conv", 333, "parem", "grid")])
+def test_find_options(parem, torch_mod, kernel, L, cand, boundary):
+    c = synth.config(3 if kernel != "auto" else 2, n=700_001)
+    x = c.make_input()
+    check_find(parem, torch_mod, c.table, c.start, c.accept, x,
+               parem.options(chunk_len=L, candidates=cand, boundary=boundary, kernel=kernel), offset=L % 16)
+
+
+def test_find_caps_partial_and_paper_example(parem, torch_mod):
+    """Caps keep the first offsets; partial tables stop at DEAD; the worked example's one
+    occurrence of "parallel" ends at offset 12."""
+    c = synth.config(2, n=1 << 20)
+    x = c.make_input()
+    for cap in (0, 1, 7, 50):
+        check_find(parem, torch_mod, c.table, c.start, c.accept, x, cap=cap)
+    rng = np.random.default_rng(5)
+    for seed in range(6):
+        t = synth.partial_dfa(int(rng.choice([5, 40, 300])), 4, 0.02, seed, np.uint16)
+        acc = rng.random(t.shape[0]) < 0.4
+        x = rng.integers(0, 4, 200_000).astype(np.uint8)
+        check_find(parem, torch_mod, t, 0, acc, x, parem.options(chunk_len=int(rng.choice([0, 100]))))
+    t = synth.kmp_dfa([0, 1, 2, 1, 4, 4, 3, 4], 5, np.uint32)
+    acc = np.zeros(9, dtype=bool)
+    acc[8] = True
+    x = np.array(["parel".index(ch) for ch in "plaraparallelapareparapl"], np.uint8)
+    r = check_find(parem, torch_mod, t, 0, acc, x, parem.options(chunk_len=6, boundary="grid"))
+    with parem.Dfa(t, 0, acc) as d:
+        _, pos = d.find(to_dev(torch_mod, x))
+    assert pos.tolist() == [12] and r.match_count == 1
