@@ -210,6 +210,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-micro", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-find", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=64 << 20)
     ap.add_argument("--verify", action="store_true", help="bit-exact check against the oracle (full size)")
     args = ap.parse_args()
@@ -350,6 +351,36 @@ def main():
                          "bytes_per_buffer": n, "ms_per_graph": round(gms, 4),
                          "us_per_match": round(1e3 * gms / K, 3), "last_count": rg.match_count}
 
+    # ---- NEXT-4: match positions (parem_find_async) on the same input, a few steps ----
+    find = None
+    if not args.no_find:
+        fws = torch.zeros(dfa.find_workspace_bytes(n, opts), dtype=torch.uint8, device=dev)
+        cap = max(1024, min(n, 1 << 26))
+        fpos = torch.empty(cap, dtype=torch.int64, device=dev)
+        fres = torch.zeros(64, dtype=torch.uint8, device=dev)
+        for _ in range(2):
+            dfa.find_async(xd, fws, fpos, fres, opts, stream)
+        torch.cuda.synchronize()
+        fsteps = max(1, min(args.steps, 5))
+        P.profile(True)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(fsteps):
+            dfa.find_async(xd, fws, fpos, fres, opts, stream)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        P.profile(False)
+        frecs = P.profile_read()
+        fk = {}
+        for _, name, ms in frecs:
+            fk.setdefault(name, []).append(ms)
+        fms = reduce_max(f0.elapsed_time(f1) / fsteps, dist, dev)
+        fr = P.MatchResult.from_bytes(fres.cpu().numpy().tobytes()[:56])
+        assert fr.match_count == r.match_count
+        find = {"value": round(n * ws_ / (fms * 1e-3) / 1e9, 2), "unit": UNIT, "ms_per_step": round(fms, 4),
+                "positions": int(fr.match_count), "kernels_ms": {k: round(statistics.median(v), 4) for k, v in fk.items()},
+                "note": "parem_find_async: the match plus every match end offset (NEXT-4)"}
+
     clocks = clk.summary()
     kernel_ms = kern_med[dominant]
     W_exec = r.route_steps / n
@@ -416,6 +447,7 @@ def main():
         "e2e": e2e,
         "micro": micro,
         "graph_batched": graph_batched,
+        "find": find,
     }
     if not args.no_cpu_baseline and rank == 0 and ws_ == 1:
         line["cpu_baseline"] = cpu_baseline(cfg, x)
