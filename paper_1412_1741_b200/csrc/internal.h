@@ -85,6 +85,8 @@ struct MatchParams {
     uint32_t* fmhits;          // tiny: per-chunk dense maps (hits) [p][Qpad]
     uint32_t* fgend;           // tiny: per-group maps (end) [groups][Qpad]
     unsigned long long* fghits;        // tiny: per-group maps (hits)
+    uint32_t* fsend;           // tiny: per-super-group maps (end) [groups/32][Qpad]
+    uint32_t* fsq;             // tiny: entering state per super-group
 };
 
 struct Plan {

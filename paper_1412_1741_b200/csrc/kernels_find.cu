@@ -42,25 +42,49 @@ __global__ void __launch_bounds__(kFindThreads) find_group_kernel(const MatchPar
     }
 }
 
-// ---- tiny path: one warp walks the group maps along q0's path (shuffles, lane = state);
-// the maps of 32 groups are loaded at once so the loads overlap ----
+// ---- tiny path: super-groups of 32 groups (1024 chunks): warp per super-group composes its
+// group maps (lane = state) into a super map (end only), then ONE warp walks the super maps
+// along q0's path, then every super-group's warp walks its 32 groups from its entering state
+__global__ void __launch_bounds__(kFindThreads) find_super_kernel(const MatchParams P, uint64_t groups) {
+    const uint64_t sg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31u, Qpad = P.d.Qpad;
+    const uint64_t nsg = (groups + 31) / 32;
+    if (sg >= nsg) return;
+    uint32_t ce = lane < Qpad ? lane : 0;
+    const uint64_t lo = sg * 32, hi = min(groups, lo + 32);
+    for (uint64_t g = lo; g < hi; ++g) ce = P.fgend[g * Qpad + ce];
+    if (lane < Qpad) P.fsend[sg * Qpad + lane] = ce;
+}
+
 __global__ void find_group_seq_kernel(const MatchParams P, uint64_t groups) {
     const uint32_t lane = threadIdx.x & 31u, Qpad = P.d.Qpad;
     if (threadIdx.x >= 32) return;
+    const uint64_t nsg = (groups + 31) / 32;
     bool dead;
     uint32_t q = start_state(P, &dead);
-    for (uint64_t g0 = 0; g0 < groups; g0 += 32) {
+    for (uint64_t s0 = 0; s0 < nsg; s0 += 32) {   // the maps of 32 super-groups load at once
         uint32_t e[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-            e[j] = (g0 + j < groups && lane < Qpad) ? P.fgend[(g0 + j) * Qpad + lane] : 0u;
+        for (int j = 0; j < 32; ++j) e[j] = (s0 + j < nsg && lane < Qpad) ? P.fsend[(s0 + j) * Qpad + lane] : 0u;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            if (g0 + j < groups) {
-                if (lane == 0) P.fgq[g0 + j] = q;   // entering state of group g0 + j
+        for (int j = 0; j < 32; ++j)
+            if (s0 + j < nsg) {
+                if (lane == 0) P.fsq[s0 + j] = q;
                 q = __shfl_sync(0xFFFFFFFFu, e[j], q);
             }
-        }
+    }
+}
+
+__global__ void __launch_bounds__(kFindThreads) find_group_in_kernel(const MatchParams P, uint64_t groups) {
+    const uint64_t sg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nsg = (groups + 31) / 32;
+    if (sg >= nsg || lane != 0) return;
+    uint32_t q = P.fsq[sg];
+    const uint64_t lo = sg * 32, hi = min(groups, lo + 32);
+    for (uint64_t g = lo; g < hi; ++g) {
+        P.fgq[g] = q;
+        q = P.fgend[g * P.d.Qpad + q];
     }
 }
 
@@ -180,8 +204,10 @@ __global__ void __launch_bounds__(kFindThreads) find_emit_tiny_kernel(const Matc
     };
     uint64_t a = b0;
     for (; a < b1 && (((uintptr_t)(P.in + a)) & 15u); ++a) step(P.in[a], a);
+    uint4 nx = a + 16 <= b1 ? ldg_v4_na(P.in + a) : make_uint4(0, 0, 0, 0);
     for (; a + 16 <= b1; a += 16) {
-        const uint4 x = ldg_v4_na(P.in + a);
+        const uint4 x = nx;
+        if (a + 32 <= b1) nx = ldg_v4_na(P.in + a + 16);
         const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q)
@@ -191,21 +217,39 @@ __global__ void __launch_bounds__(kFindThreads) find_emit_tiny_kernel(const Matc
     for (; a < b1; ++a) step(P.in[a], a);
 }
 
-// symbol-major lanes tables (entry = dest * ES | acc << (8 ES - 1)), global / L2
-template <bool W32>
+// symbol-major lanes tables (entry = dest * ES | acc << (8 ES - 1)): shared memory when the
+// table fits (SMEM), else global / L2
+template <bool W32, bool SMEM>
 __global__ void __launch_bounds__(kFindThreads) find_emit_lanes_kernel(const MatchParams P) {
+    extern __shared__ __align__(16) unsigned char sm[];
     const DevDfa& d = P.d;
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= P.p) return;
     constexpr uint32_t ES = W32 ? 4 : 2, ACC = W32 ? 31 : 15;
     const uint32_t COL = d.Qpad * ES, SMASK = (d.Qpad - 1u) * ES, CMASK = d.Apad - 1u;
     const unsigned char* g = reinterpret_cast<const unsigned char*>(d.lanes_tab);
+    uint32_t sbase = 0;
+    if (SMEM) {   // staged at a multiple of the column stride: the base ORs into offsets
+        const uint32_t sraw = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+        sbase = (sraw + COL - 1) / COL * COL;
+        const size_t bytes = (size_t)d.Apad * COL;
+        const uint4* src = reinterpret_cast<const uint4*>(d.lanes_tab);
+        uint4* dst = reinterpret_cast<uint4*>(sm + (sbase - sraw));
+        for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+        __syncthreads();
+    }
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= P.p) return;
     const uint64_t b0 = find_b(P, t), b1 = find_b(P, t + 1);
     uint32_t e = P.fchunk_q[t] * ES;
     unsigned long long o = P.fchunk_base[t];
     auto step = [&](uint32_t c, uint64_t k) {
-        const uint32_t off = (e & SMASK) | ((c & CMASK) * COL);
-        e = W32 ? __ldg(reinterpret_cast<const uint32_t*>(g + off)) : __ldg(reinterpret_cast<const uint16_t*>(g + off));
+        const uint32_t off = (e & SMASK) | ((c & CMASK) * COL + sbase);
+        if constexpr (SMEM) {
+            if constexpr (W32) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(off));
+            else asm volatile("ld.shared.u16 %0, [%1];" : "=r"(e) : "r"(off));
+        } else {
+            e = W32 ? __ldg(reinterpret_cast<const uint32_t*>(g + off))
+                    : __ldg(reinterpret_cast<const uint16_t*>(g + off));
+        }
         if (e >> ACC) {
             if (o < P.fmax) P.fout[o] = k;
             ++o;
@@ -213,8 +257,10 @@ __global__ void __launch_bounds__(kFindThreads) find_emit_lanes_kernel(const Mat
     };
     uint64_t a = b0;
     for (; a < b1 && (((uintptr_t)(P.in + a)) & 15u); ++a) step(P.in[a], a);
+    uint4 nx = a + 16 <= b1 ? ldg_v4_na(P.in + a) : make_uint4(0, 0, 0, 0);
     for (; a + 16 <= b1; a += 16) {
-        const uint4 x = ldg_v4_na(P.in + a);
+        const uint4 x = nx;
+        if (a + 32 <= b1) nx = ldg_v4_na(P.in + a + 16);
         const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q)
@@ -234,9 +280,10 @@ size_t find_extra_bytes(const Plan& plan, const DevDfa& d) {
     const uint64_t p = plan.p, groups = (p + kGroup - 1) / kGroup, nb = (p + kScanBlock - 1) / kScanBlock;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     size_t s = al(4 * p) + al(4 * p) + al(8 * p) + al(8 * nb) + al(4 * groups);
+    const uint64_t nsg = (groups + 31) / 32;
     if (plan.kernel == kKernelTiny)
         s += al((size_t)p * d.Qpad) + al(4 * (size_t)p * d.Qpad) + al(4 * (size_t)groups * d.Qpad) +
-             al(8 * (size_t)groups * d.Qpad);
+             al(8 * (size_t)groups * d.Qpad) + al(4 * (size_t)nsg * d.Qpad) + al(4 * nsg);
     return s;
 }
 
@@ -254,6 +301,9 @@ void find_bind(const Plan& plan, MatchParams& P, unsigned char* extra) {
         P.fmhits = reinterpret_cast<uint32_t*>(o); o += al(4 * (size_t)p * P.d.Qpad);
         P.fgend = reinterpret_cast<uint32_t*>(o); o += al(4 * (size_t)groups * P.d.Qpad);
         P.fghits = reinterpret_cast<unsigned long long*>(o); o += al(8 * (size_t)groups * P.d.Qpad);
+        const uint64_t nsg = (groups + 31) / 32;
+        P.fsend = reinterpret_cast<uint32_t*>(o); o += al(4 * (size_t)nsg * P.d.Qpad);
+        P.fsq = reinterpret_cast<uint32_t*>(o); o += al(4 * nsg);
     }
 }
 
@@ -262,7 +312,10 @@ int launch_find(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     if (plan.kernel == kKernelTiny) {
         find_group_kernel<<<nblk(groups * 32, kFindThreads), kFindThreads, 0, s>>>(P, groups);
         prof_after("find_group", s);
+        const uint64_t nsg = (groups + 31) / 32;
+        find_super_kernel<<<nblk(nsg * 32, kFindThreads), kFindThreads, 0, s>>>(P, groups);
         find_group_seq_kernel<<<1, 32, 0, s>>>(P, groups);
+        find_group_in_kernel<<<nblk(nsg * 32, kFindThreads), kFindThreads, 0, s>>>(P, groups);
         find_chunks_kernel<<<nblk(groups, kFindThreads), kFindThreads, 0, s>>>(P, groups);
         prof_after("find_resolve", s);
     } else if (plan.kernel == kKernelLanes) {
@@ -276,10 +329,17 @@ int launch_find(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     if (plan.kernel == kKernelTiny) {
         const size_t smem = (size_t)P.d.Qp * P.d.A * 2;
         find_emit_tiny_kernel<<<nblk(p, kFindThreads), kFindThreads, smem, s>>>(P);
-    } else if (P.d.lanes_u32) {
-        find_emit_lanes_kernel<true><<<nblk(p, kFindThreads), kFindThreads, 0, s>>>(P);
     } else {
-        find_emit_lanes_kernel<false><<<nblk(p, kFindThreads), kFindThreads, 0, s>>>(P);
+        const size_t ES = P.d.lanes_u32 ? 4 : 2, tb = (size_t)P.d.Apad * P.d.Qpad * ES;
+        const bool smem = tb <= (size_t)160 * 1024;
+        const size_t sm = smem ? tb + (size_t)P.d.Qpad * ES : 0;   // + alignment slack
+        const void* fn = P.d.lanes_u32 ? (smem ? (const void*)find_emit_lanes_kernel<true, true>
+                                               : (const void*)find_emit_lanes_kernel<true, false>)
+                                       : (smem ? (const void*)find_emit_lanes_kernel<false, true>
+                                               : (const void*)find_emit_lanes_kernel<false, false>);
+        if (smem) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        void* args[] = {const_cast<MatchParams*>(&P)};
+        cudaLaunchKernel(fn, dim3(nblk(p, kFindThreads)), dim3(kFindThreads), args, sm, s);
     }
     prof_after("find_emit", s);
     const cudaError_t e = cudaGetLastError();
