@@ -147,14 +147,13 @@ struct Routes {
                                          const uint16_t* __restrict__ tab1, uint32_t A, uint32_t badmask,
                                          uint32_t lane4) {
         if constexpr (B == 2) {
-            bad |= w & badmask;
+            // (invalid bytes are flagged per 16-byte vector in vec())
             // w * 130 = w<<7 + w<<1: b0 | b1<<2 lands in bits 7..10 and b2 | b3<<2 in bits
             // 23..26; every other partial product has its own 2-bit slot (no carries).
             const uint32_t P = w * 130u;
             group(P & 0x780u, tabk);                         // symbols 0,1
             group(__umulhi(w, 0x00820000u) & 0x780u, tabk);  // symbols 2,3: (w * 130) >> 16 on the FMA pipe
         } else if constexpr (B == 1) {
-            bad |= w & badmask;
             const uint32_t P = w * 0x10204080u;  // b0..b3 -> bits 28..31
             group((P >> 21) & 0x780u, tabk);
         } else {
@@ -169,6 +168,7 @@ struct Routes {
     __device__ __forceinline__ void vec(const uint4& x, const unsigned char* __restrict__ tabk,
                                         const uint16_t* __restrict__ tab1, uint32_t A, uint32_t badmask,
                                         uint32_t lane4) {
+        if constexpr (B != 0) bad |= (x.x | x.y | x.z | x.w) & badmask;   // bytes >= A (C11)
         word(x.x, tabk, tab1, A, badmask, lane4);
         word(x.y, tabk, tab1, A, badmask, lane4);
         word(x.z, tabk, tab1, A, badmask, lane4);
