@@ -181,11 +181,14 @@ def run_reference(args):
     return 0
 
 
-def latest_traffic(cfg_index: int):
-    """dram bytes per launch from the committed ncu --set full summary, if any."""
+def latest_traffic(cfg_index: int, kernel: str = ""):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary, if any
+    (profiles/r*_ncu_full_cfg<k>.json for the tiny kernel, ..._cfg<k>_follow.json for
+    conv_follow)."""
     import glob
 
-    cands = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_full_cfg{cfg_index}.json")))
+    suffix = "_follow" if kernel == "conv_follow" else ""
+    cands = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_full_cfg{cfg_index}{suffix}.json")))
     if not cands:
         return None
     try:
@@ -415,7 +418,7 @@ def main():
                  "peak_source": "148 SMs x 32 lookups/clk x sm_max_mhz",
                  "units_per_launch": f"{r.route_steps} route-steps"}
     bound["frac"] = round(bound["achieved"] / bound["peak"], 4)
-    bound["traffic"] = latest_traffic(cfg.index)
+    bound["traffic"] = latest_traffic(cfg.index, bound.get("kernel", dominant))
     bound["kernel_ms"] = round(kernel_ms, 4)
     bound.setdefault("kernel", dominant)
     bound["dominant_kernel"] = dominant
