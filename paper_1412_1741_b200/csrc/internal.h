@@ -136,7 +136,7 @@ int launch_conv(const Plan& plan, const MatchParams& P, cudaStream_t s);
 int launch_find(const Plan& plan, const MatchParams& P, cudaStream_t s);
 size_t find_extra_bytes(const Plan& plan, const DevDfa& d);
 void find_bind(const Plan& plan, MatchParams& P, unsigned char* extra);
-size_t conv_chunk_bytes();
+size_t conv_ws_total(uint64_t p);
 size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap);
 int launch_trivial(const MatchParams& P, cudaStream_t s);
 int tiny_blocks_per_sm(uint32_t K, uint32_t B, bool tma, size_t smem);

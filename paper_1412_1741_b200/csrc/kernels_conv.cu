@@ -7,18 +7,19 @@
 // sequential ones exactly: the per-chunk map start -> (end, hits) is never approximated,
 // it is evaluated at the one start state the join needs.
 //
-// Four launches per match (all graph-capturable):
-//   K1 conv_set    warp per chunk: walk the SET R_i (deduplicated each step) until at most
-//                  kDMax distinct states remain at offset m_i (or the chunk ends: "open");
-//   K2 conv_follow thread per chunk: walk the <= kDMax survivors z_k over the rest of the
-//                  chunk -> (end_k, tail hits_k); all routes equal at the end = "anchor"
-//                  (the chunk's end state is then independent of its start state);
-//   J  conv_join   one CTA: the true state q_i at every boundary -- q_{i+1} = end of an
-//                  anchor chunk, otherwise walk the head from q_i and pick z_k -- with
-//                  segment-parallel passes (only anchor-free runs are sequential);
-//   K3 conv_heads  thread per chunk: walk q_i over the head [b_i, b_i + m_i) -> z_k and the
-//                  head hits; chunk hits = head + tail_k; last CTA writes the result.
-// Every input byte is read by K2 (tails) or K3 (heads) and validated there (reading C11).
+// Launches per match (all graph-capturable):
+//   K1 conv_set     warp per chunk: walk the SET R_i (deduplicated each step) until at most
+//                   dmax distinct states remain at offset m_i (hand-over); if the chunk ends
+//                   first, its <= 32 phase-B states are the survivors, walked to the end
+//                   ("open"); a set that never shrank to 32 states is "wide";
+//   K2 conv_follow  thread per chunk: walk the <= 4 handed-over survivors z_k over the rest
+//                   of the chunk -> (end_k, tail hits_k);
+//   E1..E5          the join as a composition of small maps: each chunk's end set (<= 32
+//                   states, 1 once its routes merged), each chunk as a map from the previous
+//                   end set (head walks, lanes of a warp), block composition, one warp along
+//                   q0's path, per-chunk resolution and the result.  Only wide chunks fall
+//                   back to one sequential thread.
+// Every input byte is validated once (reading C11): K2 tails, E2 heads and open tails.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -45,11 +46,71 @@ struct ConvChunk {      // 64 B per chunk in the workspace
 };
 static_assert(sizeof(ConvChunk) == 64, "ConvChunk");
 
+// Survivors of a chunk once its set walk has shrunk to <= 32 states: z[k] at offset m (the
+// head), walked to the chunk end -> end[k], tail hits tail[k]; eidx[k] = index of end[k] in
+// the chunk's end set.  Every chunk has one (n = 0 only for a "wide" chunk whose set never
+// shrank to 32 states).
+constexpr uint32_t kMaxSurv = 32;
+constexpr uint32_t kWide = 0xFFFFFFFFu;
+struct SurvRec {
+    uint32_t n;
+    uint32_t z[kMaxSurv];
+    uint32_t end[kMaxSurv];
+    uint32_t tail[kMaxSurv];
+    uint8_t eidx[kMaxSurv];
+    uint32_t pad;
+};
+struct EndSet {        // distinct end states of a chunk (the possible entering states of the next)
+    uint32_t n;
+    uint32_t s[kMaxSurv];
+    uint32_t pad;
+};
+struct MapRec {        // chunk i as a map over the end set of chunk i-1 (entering index j)
+    uint8_t idx[kMaxSurv];     // -> index into this chunk's end set
+    uint32_t hits[kMaxSurv];   // hits of the walk through this chunk
+};
+constexpr uint32_t kBlk = 32;   // chunks per composed block
+struct BlockMap {
+    uint8_t idx[kMaxSurv];
+};
+
+struct ConvWs {        // the converging path's workspace after the 256-byte header area
+    ConvChunk* info;
+    SurvRec* surv;
+    EndSet* ends;
+    MapRec* maps;
+    BlockMap* bmaps;
+    uint32_t* bin;     // entering index per block (+ the final index at [nblocks])
+};
+
+__host__ __device__ __forceinline__ size_t alw(size_t x) { return (x + 255) & ~(size_t)255; }
+
+__host__ __device__ __forceinline__ size_t conv_ws_bytes(uint64_t p) {
+    const uint64_t nb = (p + kBlk - 1) / kBlk;
+    return alw(p * sizeof(ConvChunk)) + alw(p * sizeof(SurvRec)) + alw(p * sizeof(EndSet)) +
+           alw(p * sizeof(MapRec)) + alw(nb * sizeof(BlockMap)) + alw(4 * (nb + 1));
+}
+
+__device__ __forceinline__ ConvWs conv_ws(const MatchParams& P) {
+    const uint64_t p = P.p, nb = (p + kBlk - 1) / kBlk;
+    unsigned char* o = reinterpret_cast<unsigned char*>(P.maps);
+    ConvWs w;
+    w.info = reinterpret_cast<ConvChunk*>(o); o += alw(p * sizeof(ConvChunk));
+    w.surv = reinterpret_cast<SurvRec*>(o); o += alw(p * sizeof(SurvRec));
+    w.ends = reinterpret_cast<EndSet*>(o); o += alw(p * sizeof(EndSet));
+    w.maps = reinterpret_cast<MapRec*>(o); o += alw(p * sizeof(MapRec));
+    w.bmaps = reinterpret_cast<BlockMap*>(o); o += alw(nb * sizeof(BlockMap));
+    w.bin = reinterpret_cast<uint32_t*>(o);
+    return w;
+}
+
 __host__ __device__ __forceinline__ size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 // K1 per-warp scratch: the candidate list (u16 state indices, compacted in place) and a
 // |Q|-bit image bitmap.
+constexpr int kPark = 4;   // parked chunks per warp in the set walk's phase B
 __host__ __device__ __forceinline__ size_t set_warp_bytes(uint32_t cap, uint32_t Qpad) {
+    // list | image bitmap | parked slots: start state per lane, D and phase-B start offset
     return al16(2 * (size_t)cap) + al16((size_t)(Qpad + 31) / 32 * 4);
 }
 
@@ -120,8 +181,6 @@ __device__ __forceinline__ uint64_t conv_b(const MatchParams& P, uint64_t i) {
 // advances all its parked chunks together, 32 bytes at a time -- kPark independent lookup
 // chains per lane -- counting distinct states with __match_any_sync, until <= dmax remain
 // (hand-over) or the chunk ends (open).  A freed slot is refilled by the next chunk's phase A.
-constexpr int kPark = 4;
-
 template <bool SMEM, bool W32>
 __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchParams P) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -139,15 +198,35 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
     const uint8_t* in = P.in;
     const uint32_t ltmask = (1u << lane) - 1u;
     const uint32_t dmax = P.dmax;
-    ConvChunk* infos = reinterpret_cast<ConvChunk*>(P.maps);
+    const ConvWs W = conv_ws(P);
+    ConvChunk* infos = W.info;
 
     auto distinct = [&](uint32_t e, uint32_t& leaders) {
         const uint32_t m = __match_any_sync(0xFFFFFFFFu, T.state(e));
         leaders = __ballot_sync(0xFFFFFFFFu, (__ffs(m) - 1) == (int)lane);
         return (uint32_t)__popc(leaders);
     };
-    auto write_open = [&](uint64_t t, uint64_t b0, uint64_t b1) {
+    // a chunk whose set never shrank to 32 states: no survivors (sequential fallback)
+    auto write_wide = [&](uint64_t t, uint64_t b0, uint64_t b1) {
         if (lane == 0) {
+            infos[t].m = (uint32_t)(b1 - b0);
+            infos[t].D = kWide;
+            W.surv[t].n = 0;
+        }
+    };
+    // open chunk (routes did not merge to <= dmax by its end): the survivors are its <= 32
+    // distinct END states and its head is the whole chunk (the join walks it from each
+    // possible entering state)
+    auto write_open = [&](uint64_t t, uint64_t b0, uint64_t b1, uint32_t e, uint32_t leaders, uint32_t nd) {
+        SurvRec& s = W.surv[t];
+        if ((leaders >> lane) & 1u) {
+            const uint32_t r = __popc(leaders & ltmask);
+            s.z[r] = T.state(e);
+            s.end[r] = T.state(e);
+            s.tail[r] = 0;
+        }
+        if (lane == 0) {
+            s.n = nd;
             infos[t].m = (uint32_t)(b1 - b0);
             infos[t].D = 0;
         }
@@ -228,7 +307,7 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
                 ++pos;
             }
             if (D > 32) {   // reached the chunk end in phase A
-                write_open(t, b0, b1);
+                write_wide(t, b0, b1);
                 continue;
             }
             const uint32_t e = (lane < D ? list[lane] : list[0]) * T.ES;
@@ -239,7 +318,7 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
                 continue;
             }
             if (pos >= b1) {
-                write_open(t, b0, b1);
+                write_open(t, b0, b1, e, leaders, nd);
                 continue;
             }
             const int k = __ffs(~occ) - 1;   // park it
@@ -280,7 +359,7 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
                 write_handover(pt[j], ppos[j] - pb0[j], pe[j], leaders, nd);
                 occ &= ~(1u << j);
             } else if (ppos[j] >= pb1[j]) {
-                write_open(pt[j], pb0[j], pb1[j]);
+                write_open(pt[j], pb0[j], pb1[j], pe[j], leaders, nd);
                 occ &= ~(1u << j);
             }
         }
@@ -335,9 +414,11 @@ __global__ void __launch_bounds__(kFollowThreads) conv_follow_kernel(const Match
     __syncthreads();
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = t < P.p;
-    ConvChunk* info = reinterpret_cast<ConvChunk*>(P.maps) + (live ? t : 0);
+    const ConvWs W = conv_ws(P);
+    ConvChunk* info = W.info + (live ? t : 0);
     const uint64_t b0 = conv_b(P, t), b1 = live ? conv_b(P, t + 1) : b0;
-    const uint32_t D = live ? info->D : 0u;
+    const uint32_t D0 = live ? info->D : 0u;
+    const uint32_t D = D0 == kWide ? 0u : D0;   // follow only handed-over chunks
     const bool act = D != 0;
     uint64_t a = act ? b0 + info->m : b1;
     uint32_t e[kDMax], h[kDMax];
@@ -397,14 +478,15 @@ __global__ void __launch_bounds__(kFollowThreads) conv_follow_kernel(const Match
         stepK(c);
     }
     if (!act) return;
-    bool anchor = true;
+    SurvRec& sr = W.surv[t];
+    sr.n = D;
 #pragma unroll
-    for (int k = 0; k < (int)kDMax; ++k) {
-        info->end[k] = T.state(e[k]);
-        info->tail[k] = h[k];
-        anchor &= T.state(e[k]) == T.state(e[0]);
-    }
-    info->anchor = anchor;
+    for (int k = 0; k < (int)kDMax; ++k)
+        if ((uint32_t)k < D) {
+            sr.z[k] = info->z[k];
+            sr.end[k] = T.state(e[k]);
+            sr.tail[k] = h[k];
+        }
     if (bad) {
         const uint64_t off = first_bad(in, b0 + info->m, b1, A);
         if (off < b1) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
@@ -443,133 +525,294 @@ __device__ __forceinline__ uint32_t walk1(const DevDfa& d, const uint8_t* in, ui
     return T.state(e);
 }
 
-// The state after chunk i given the state q at its start.
-template <bool W32>
-__device__ __forceinline__ uint32_t conv_advance(const MatchParams& P, const ConvChunk* info, uint64_t i, uint32_t q,
-                                                 uint32_t* err) {
-    const ConvChunk& c = info[i];
-    if (c.D != 0 && c.anchor) return c.end[0];
-    const uint64_t b0 = conv_b(P, i);
-    const uint32_t z = walk1<W32>(P.d, P.in, b0, b0 + c.m, q, nullptr);
-    if (c.D == 0) return z;   // open chunk: the head is the whole chunk
-    for (uint32_t k = 0; k < c.D; ++k)
-        if (c.z[k] == z) return c.end[k];
-    *err = 1;   // speculation unsound: the true state is not among the survivors
-    return z;
-}
-
 // ---------------------------------------------------------------------------------------
-// J: the true state q_i at every boundary (the join).  Thread per chunk:
-// q_i = end of the nearest anchor chunk a < i (its end does not depend on its start),
-// advanced through the non-anchor chunks a+1 .. i-1 (head walk + survivor pick).  A chunk
-// with no anchor among its kJoinBack predecessors is left to conv_join_seq_kernel, which
-// runs the whole chain on one thread only when some chunk needed it.
-constexpr uint32_t kJoinBack = 128;
-constexpr uint32_t kUnresolved = 0xFFFFFFFFu;
+// The join, as a composition of SMALL maps.  Chunk i's possible entering
+// states are the end set of chunk i-1 (<= 32 states; 1 when its routes merged).  E2 walks
+// each of them over chunk i's head [b_i, b_i + m_i) (lanes of one warp, same bytes),
+// matches the state reached against chunk i's survivors and so turns chunk i into a map
+// "entering index -> (end-set index, hits)".  E3 composes blocks of 32 such maps (lane =
+// entering index), E4 walks the block maps along q0's path, E5 resolves every chunk's
+// entering state and hits in parallel and writes the result.  Every step is parallel
+// whether or not routes merged; only "wide" chunks (the set never shrank to 32 states)
+// fall back to one sequential thread (conv_seq_kernel).
 
-template <bool W32>
-__global__ void __launch_bounds__(kFollowThreads) conv_join_kernel(const MatchParams P) {
-    ConvChunk* info = reinterpret_cast<ConvChunk*>(P.maps);
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P.p) return;
-    uint32_t err = 0, q = kUnresolved;
-    uint64_t a = i;   // first chunk to advance through
-    bool dead;
-    if (i == 0) q = start_state(P, &dead);
-    else {
-        const uint64_t lo = i > kJoinBack ? i - kJoinBack : 0;
-        for (uint64_t j = i; j > lo; --j) {
-            const ConvChunk& c = info[j - 1];
-            if (c.D != 0 && c.anchor) {
-                q = c.end[0];
-                a = j;
-                break;
-            }
-        }
-        if (q == kUnresolved && lo == 0) {   // no anchor back to chunk 0: start from q0
-            q = start_state(P, &dead);
-            a = 0;
-        }
-    }
-    if (q == kUnresolved) atomicOr(&P.hdr->err, 2u);   // chain too long: sequential pass
-    else
-        for (uint64_t j = a; j < i; ++j) q = conv_advance<W32>(P, info, j, q, &err);
-    info[i].q = q;
-    if (err) atomicOr(&P.hdr->err, 1u);
-}
-
-template <bool W32>
-__global__ void conv_join_seq_kernel(const MatchParams P) {
-    if (threadIdx.x != 0 || !(P.hdr->err & 2u)) return;
-    ConvChunk* info = reinterpret_cast<ConvChunk*>(P.maps);
-    uint32_t err = 0;
-    bool dead;
-    uint32_t q = start_state(P, &dead);
-    for (uint64_t i = 0; i < P.p; ++i) {
-        info[i].q = q;
-        q = conv_advance<W32>(P, info, i, q, &err);
-    }
-    if (err) atomicOr(&P.hdr->err, 1u);
-}
-
-// ---------------------------------------------------------------------------------------
-// K3: the head of every chunk from its true state, the chunk's hits, and the result.
-template <bool W32>
-__global__ void __launch_bounds__(kFollowThreads) conv_heads_kernel(const MatchParams P) {
-    __shared__ unsigned long long acc[3];   // hits, routes, route-steps of this CTA
-    __shared__ uint32_t flag;
-    const DevDfa& d = P.d;
+// E1: end set of every chunk (distinct survivor ends) and each survivor's index in it.
+__global__ void __launch_bounds__(kFollowThreads) conv_ends_kernel(const MatchParams P) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t lane = threadIdx.x & 31u;
-    if (threadIdx.x < 3) acc[threadIdx.x] = 0;
+    if (t >= P.p) return;
+    const ConvWs W = conv_ws(P);
+    SurvRec& s = W.surv[t];
+    EndSet& es = W.ends[t];
+    if (W.info[t].D == kWide) {
+        es.n = 0;
+        atomicOr(&P.hdr->err, 2u);
+        return;
+    }
+    uint32_t n = 0;
+    for (uint32_t k = 0; k < s.n; ++k) {
+        const uint32_t v = s.end[k];
+        uint32_t j = 0;
+        while (j < n && es.s[j] != v) ++j;
+        if (j == n) es.s[n++] = v;
+        s.eidx[k] = (uint8_t)j;
+    }
+    es.n = n;
+}
+
+// E2a: chunks entered from ONE possible state (chunk 0, or the previous chunk's routes all
+// merged) -- thread per chunk: head walk, survivor pick, validation, stats.
+template <bool W32>
+__global__ void __launch_bounds__(kFollowThreads) conv_map1_kernel(const MatchParams P) {
+    __shared__ unsigned long long acc[2];
+    const DevDfa& d = P.d;
+    if (threadIdx.x < 2) acc[threadIdx.x] = 0;
     __syncthreads();
-    const ConvChunk* info = reinterpret_cast<const ConvChunk*>(P.maps);
-    unsigned long long hits = 0, rc = 0, steps = 0;
-    if (t < P.p) {
-        const ConvChunk& c = info[t];
+    const ConvWs W = conv_ws(P);
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t A = d.A;
+    unsigned long long rc = 0, steps = 0;
+    if (t < P.p && !(P.hdr->err & 2u) && (t == 0 || W.ends[t - 1].n == 1)) {
         const uint64_t b0 = conv_b(P, t), b1 = conv_b(P, t + 1);
+        const ConvChunk& c = W.info[t];
+        const SurvRec& s = W.surv[t];
+        bool dead;
+        const uint32_t q = t == 0 ? start_state(P, &dead) : W.ends[t - 1].s[0];
         uint32_t hh = 0;
-        const uint32_t z = walk1<W32>(d, P.in, b0, b0 + c.m, c.q, &hh);
-        hits = hh;
-        uint32_t fin = z;   // open chunk: the head is the whole chunk
-        if (c.D != 0) {
-            uint32_t k = 0;
-            while (k < c.D && c.z[k] != z) ++k;
-            if (k == c.D) atomicOr(&P.hdr->err, 1u);
-            else {
-                hits += c.tail[k];
-                fin = c.end[k];
-            }
+        const uint32_t z = walk1<W32>(d, P.in, b0, b0 + c.m, q, &hh);
+        uint32_t k = 0;
+        while (k < s.n && s.z[k] != z) ++k;
+        if (k == s.n) {
+            atomicOr(&P.hdr->err, 1u);   // speculation unsound: cannot happen
+            k = 0;
         }
-        if (t == P.p - 1) P.hdr->final_q = fin;
-        if (P.fchunk_q) {   // parem_find_async: entering state and hits of this chunk
-            P.fchunk_q[t] = c.q;
-            P.fchunk_h[t] = (uint32_t)hits;
-        }
-        const uint64_t off = first_bad(P.in, b0, b0 + c.m, d.A);
+        W.maps[t].idx[0] = s.eidx[k];
+        W.maps[t].hits[0] = hh + s.tail[k];
+        const uint64_t off = first_bad(P.in, b0, b0 + c.m, A);   // open chunks: m = whole chunk
         if (off < b0 + c.m) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
-        // stats: |R_t| (R_0 = {q0}) and |R_t| * len_t
-        if (t == 0) rc = 1;
-        else {
+        rc = 1;   // stats: |R_t| (R_0 = {q0}) and |R_t| * len_t
+        if (t > 0) {
             const uint32_t cl = P.in[b0 - 1];
-            const uint32_t li = (P.cand == PAREM_CANDIDATES_ENUM || cl >= d.A) ? d.A : cl;
+            const uint32_t li = (P.cand == PAREM_CANDIDATES_ENUM || cl >= A) ? A : cl;
             rc = route_count(P, cl, P.in[b0], __ldg(d.Lcnt + li));
         }
         steps = rc * (b1 - b0);
     }
-    hits = warp_sum(hits);
     rc = warp_sum(rc);
     steps = warp_sum(steps);
-    if (lane == 0) {
-        atomicAdd(acc + 0, hits);
-        atomicAdd(acc + 1, rc);
-        atomicAdd(acc + 2, steps);
+    if ((threadIdx.x & 31u) == 0 && rc) {
+        atomicAdd(acc + 0, rc);
+        atomicAdd(acc + 1, steps);
     }
     __syncthreads();
+    if (threadIdx.x == 0 && acc[0]) {
+        atomicAdd(&P.hdr->routes, acc[0]);
+        atomicAdd(&P.hdr->steps, acc[1]);
+    }
+}
+
+// E2b: chunks entered from SEVERAL possible states (the previous chunk's survivors did not
+// merge) -- warp per chunk, lane j walks the head from end-set state j over the same bytes.
+template <bool SMEM, bool W32>
+__global__ void __launch_bounds__(kSetWarps * 32) conv_map_kernel(const MatchParams P) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ unsigned long long acc[2];
+    const DevDfa& d = P.d;
+    Tab<SMEM, W32> T;
+    T.init(d, stage_table<SMEM, W32>(d, sm));
+    if (threadIdx.x < 2) acc[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const ConvWs W = conv_ws(P);
+    const uint8_t* in = P.in;
+    const uint32_t A = d.A;
+    const bool skip = (P.hdr->err & 2u) != 0;   // wide chunks: the sequential fallback resolves
+    unsigned long long routes = 0, steps = 0;
+    for (uint64_t t = (uint64_t)blockIdx.x * kSetWarps + warp; t < P.p && !skip; t += (uint64_t)gridDim.x * kSetWarps) {
+        if (t == 0) continue;
+        const uint32_t nin = W.ends[t - 1].n;
+        if (nin <= 1) continue;   // conv_map1_kernel's
+        const uint64_t b0 = conv_b(P, t), b1 = conv_b(P, t + 1);
+        const ConvChunk& c = W.info[t];
+        const SurvRec& s = W.surv[t];
+        const uint64_t hb = b0 + c.m;
+        const uint32_t q = W.ends[t - 1].s[lane < nin ? lane : 0];
+        uint32_t e = q * T.ES, h = 0;
+        bool badseen = false;
+        for (uint64_t pos = b0; pos < hb; pos += 32) {
+            const uint32_t cnt = (uint32_t)min((uint64_t)32, hb - pos);
+            const uint32_t mine = lane < cnt ? (uint32_t)__ldg(in + pos + lane) : 0u;
+            if (!badseen) {
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, lane < cnt && mine >= A);
+                if (bal) {
+                    badseen = true;
+                    if (lane == 0) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)(pos + __ffs(bal) - 1));
+                }
+            }
+            for (uint32_t k = 0; k < cnt; ++k) {
+                e = T.next(e, T.col(__shfl_sync(0xFFFFFFFFu, mine, k)));
+                h += T.hit(e);
+            }
+        }
+        if (lane < nin) {
+            const uint32_t z = T.state(e);
+            uint32_t k = 0;
+            while (k < s.n && s.z[k] != z) ++k;
+            if (k == s.n) {
+                atomicOr(&P.hdr->err, 1u);   // speculation unsound: cannot happen
+                k = 0;
+            }
+            W.maps[t].idx[lane] = s.eidx[k];
+            W.maps[t].hits[lane] = h + s.tail[k];
+        }
+        if (lane == 0) {   // stats: |R_t| and |R_t| * len_t
+            const uint32_t cl = in[b0 - 1];
+            const uint32_t li = (P.cand == PAREM_CANDIDATES_ENUM || cl >= A) ? A : cl;
+            const uint64_t rc = route_count(P, cl, in[b0], __ldg(d.Lcnt + li));
+            routes += rc;
+            steps += rc * (b1 - b0);
+        }
+    }
+    if (lane == 0 && routes) {
+        atomicAdd(acc + 0, routes);
+        atomicAdd(acc + 1, steps);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && acc[0]) {
+        atomicAdd(&P.hdr->routes, acc[0]);
+        atomicAdd(&P.hdr->steps, acc[1]);
+    }
+}
+
+// E3: compose the maps of each block of kBlk chunks (warp per block, lane = entering index).
+__global__ void __launch_bounds__(kFollowThreads) conv_block_kernel(const MatchParams P) {
+    const uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nb = (P.p + kBlk - 1) / kBlk;
+    if (b >= nb || (P.hdr->err & 2u)) return;
+    const ConvWs W = conv_ws(P);
+    const uint64_t c0 = b * kBlk, c1 = min(P.p, c0 + kBlk);
+    const uint32_t nin = c0 == 0 ? 1u : W.ends[c0 - 1].n;
+    uint32_t idx = lane < nin ? lane : 0;
+    for (uint64_t c = c0; c < c1; ++c) idx = W.maps[c].idx[idx];
+    W.bmaps[b].idx[lane] = (uint8_t)idx;
+}
+
+// E4: one warp walks the block maps along q0's path (32 block maps loaded at a time).
+__global__ void conv_path_kernel(const MatchParams P) {
+    const uint32_t lane = threadIdx.x & 31u;
+    if (threadIdx.x >= 32 || (P.hdr->err & 2u)) return;
+    const ConvWs W = conv_ws(P);
+    const uint64_t nb = (P.p + kBlk - 1) / kBlk;
+    uint32_t e = 0;
+    for (uint64_t b0 = 0; b0 < nb; b0 += 32) {
+        uint32_t v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = b0 + j < nb ? W.bmaps[b0 + j].idx[lane] : 0u;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (b0 + j < nb) {
+                if (lane == 0) W.bin[b0 + j] = e;
+                e = __shfl_sync(0xFFFFFFFFu, v[j], e);
+            }
+    }
+    if (lane == 0) {
+        W.bin[nb] = e;
+        P.hdr->final_q = W.ends[P.p - 1].s[e];
+    }
+}
+
+// Walk one route from state q over in[a, b) (global table); hits optional.
+template <bool W32>
+__device__ uint32_t walk_seq(const DevDfa& d, const uint8_t* in, uint64_t a, uint64_t b, uint32_t q, uint32_t* hits) {
+    return walk1<W32>(d, in, a, b, q, hits);
+}
+
+// Sequential fallback, only when a wide chunk exists: resolve every chunk on one thread.
+template <bool W32>
+__global__ void conv_seq_kernel(const MatchParams P) {
+    if (threadIdx.x != 0 || !(P.hdr->err & 2u)) return;
+    const ConvWs W = conv_ws(P);
+    const DevDfa& d = P.d;
+    bool dead;
+    uint32_t q = start_state(P, &dead);
+    unsigned long long hits = 0, routes = 0, steps = 0;
+    for (uint64_t i = 0; i < P.p; ++i) {
+        const uint64_t b0 = conv_b(P, i), b1 = conv_b(P, i + 1);
+        const ConvChunk& c = W.info[i];
+        uint32_t h = 0, nq;
+        if (c.D == kWide) {
+            nq = walk_seq<W32>(d, P.in, b0, b1, q, &h);
+            const uint64_t off = first_bad(P.in, b0, b1, d.A);
+            if (off < b1) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
+        } else {
+            const SurvRec& s = W.surv[i];
+            const uint32_t z = walk_seq<W32>(d, P.in, b0, b0 + c.m, q, &h);
+            uint32_t k = 0;
+            while (k < s.n && s.z[k] != z) ++k;
+            if (k == s.n) {
+                atomicOr(&P.hdr->err, 1u);
+                k = 0;
+            }
+            nq = s.end[k];
+            h += s.tail[k];
+            // heads here (an open chunk's head is all of it); tails of handed-over chunks
+            // were validated by the follow walk
+            const uint64_t off = first_bad(P.in, b0, b0 + c.m, d.A);
+            if (off < b0 + c.m) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
+        }
+        if (P.fchunk_q) {
+            P.fchunk_q[i] = q;
+            P.fchunk_h[i] = h;
+        }
+        uint64_t rc = 1;
+        if (i > 0) {
+            const uint32_t cl = P.in[b0 - 1];
+            const uint32_t li = (P.cand == PAREM_CANDIDATES_ENUM || cl >= d.A) ? d.A : cl;
+            rc = route_count(P, cl, P.in[b0], __ldg(d.Lcnt + li));
+        }
+        routes += rc;
+        steps += rc * (b1 - b0);
+        hits += h;
+        q = nq;
+    }
+    P.hdr->final_q = q;
+    P.hdr->hits = hits;
+    P.hdr->routes = routes;
+    P.hdr->steps = steps;
+}
+
+// E5: every chunk's entering state and hits (thread per block walking its kBlk maps), the
+// total, and the result (last CTA).
+__global__ void __launch_bounds__(kFollowThreads) conv_resolve_kernel(const MatchParams P) {
+    __shared__ unsigned long long acc;
+    __shared__ uint32_t flag;
+    if (threadIdx.x == 0) acc = 0;
+    __syncthreads();
+    const ConvWs W = conv_ws(P);
+    const uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t nb = (P.p + kBlk - 1) / kBlk;
+    const bool seq = (P.hdr->err & 2u) != 0;
+    unsigned long long hits = 0;
+    if (b < nb && !seq) {
+        bool dead;
+        const uint32_t q0 = start_state(P, &dead);
+        uint32_t e = W.bin[b];
+        const uint64_t c0 = b * kBlk, c1 = min(P.p, c0 + kBlk);
+        for (uint64_t c = c0; c < c1; ++c) {
+            const uint32_t h = W.maps[c].hits[e];
+            if (P.fchunk_q) {
+                P.fchunk_q[c] = c == 0 ? q0 : W.ends[c - 1].s[e];
+                P.fchunk_h[c] = h;
+            }
+            hits += h;
+            e = W.maps[c].idx[e];
+        }
+    }
+    hits = warp_sum(hits);
+    if ((threadIdx.x & 31u) == 0 && hits) atomicAdd(&acc, hits);
+    __syncthreads();
     if (threadIdx.x == 0) {
-        atomicAdd(&P.hdr->hits, acc[0]);
-        atomicAdd(&P.hdr->routes, acc[1]);
-        atomicAdd(&P.hdr->steps, acc[2]);
+        if (acc) atomicAdd(&P.hdr->hits, acc);
         __threadfence();
         flag = atomicAdd(&P.hdr->done, 1u) == gridDim.x - 1;
     }
@@ -599,11 +842,12 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(conv_set_kernel<SMEM, W32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(conv_follow_kernel<SMEM, W32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(conv_map_kernel<SMEM, W32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb);
     if (!SMEM && e == cudaSuccess) {
         // global (L2-resident) tables: give the unified L1/shared array to L1
         cudaFuncSetAttribute(conv_follow_kernel<SMEM, W32>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-        cudaFuncSetAttribute(conv_heads_kernel<W32>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-        cudaFuncSetAttribute(conv_join_kernel<W32>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+
     }
     if (e != cudaSuccess) {
         set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -621,12 +865,20 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     prof_after("conv_set", s);
     conv_follow_kernel<SMEM, W32><<<g2, kFollowThreads, tb, s>>>(P);
     prof_after("conv_follow", s);
-    conv_join_kernel<W32><<<g2, kFollowThreads, 0, s>>>(P);
+    conv_ends_kernel<<<g2, kFollowThreads, 0, s>>>(P);
+    int bpm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, conv_map_kernel<SMEM, W32>, kSetWarps * 32, tb);
+    if (bpm < 1) bpm = 1;
+    const unsigned gm = (unsigned)(g1w < (uint64_t)sms * bpm ? g1w : (uint64_t)sms * bpm);
+    conv_map1_kernel<W32><<<g2, kFollowThreads, 0, s>>>(P);
+    conv_map_kernel<SMEM, W32><<<gm, kSetWarps * 32, tb, s>>>(P);
+    const uint64_t nb = (P.p + kBlk - 1) / kBlk;
+    conv_block_kernel<<<(unsigned)((nb * 32 + kFollowThreads - 1) / kFollowThreads), kFollowThreads, 0, s>>>(P);
+    conv_path_kernel<<<1, 32, 0, s>>>(P);
+    conv_seq_kernel<W32><<<1, 32, 0, s>>>(P);
     prof_after("conv_join", s);
-    conv_join_seq_kernel<W32><<<1, 32, 0, s>>>(P);
-    prof_after("conv_join_seq", s);
-    conv_heads_kernel<W32><<<g2, kFollowThreads, 0, s>>>(P);
-    prof_after("conv_heads", s);
+    conv_resolve_kernel<<<(unsigned)((nb + kFollowThreads - 1) / kFollowThreads), kFollowThreads, 0, s>>>(P);
+    prof_after("conv_resolve", s);
     e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_error("conv kernels: %s", cudaGetErrorString(e));
@@ -637,7 +889,7 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
 
 }  // namespace
 
-size_t conv_chunk_bytes() { return sizeof(ConvChunk); }
+size_t conv_ws_total(uint64_t p) { return conv_ws_bytes(p); }
 
 size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap) {
     return smem_tab_bytes(d, smem_tab) + kSetWarps * set_warp_bytes(cap, d.Qpad);

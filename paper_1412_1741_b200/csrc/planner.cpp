@@ -164,7 +164,7 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         plan->smem = conv_set_smem_bytes(d, conv_smem_tab, conv_cap);
         plan->off_maps = 256;
         plan->off_hits = 0;
-        plan->ws = al256(plan->off_maps + p * conv_chunk_bytes());
+        plan->ws = al256(plan->off_maps + conv_ws_total(p));
         if (p > 0x7FFFFFFFull) { set_error("too many chunks"); return PAREM_EINVAL; }
         return PAREM_OK;
     }

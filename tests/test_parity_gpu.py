@@ -388,7 +388,7 @@ def test_profile_records_kernels(parem, torch_mod):
         parem.profile(False)
         recs = parem.profile_read()
     names = [r[1] for r in recs]
-    assert names == ["conv_set", "conv_follow", "conv_join", "conv_join_seq", "conv_heads"] * 2
+    assert names == ["conv_set", "conv_follow", "conv_join", "conv_resolve"] * 2
     assert {r[0] for r in recs} == {0, 1} and all(r[2] > 0 for r in recs)
 
 
@@ -443,3 +443,25 @@ def test_find_caps_partial_and_paper_example(parem, torch_mod):
     with parem.Dfa(t, 0, acc) as d:
         _, pos = d.find(to_dev(torch_mod, x))
     assert pos.tolist() == [12] and r.match_count == 1
+
+
+@pytest.mark.parametrize("k", [3, 4, 5])
+@pytest.mark.parametrize("kind", ["zeros", "period3", "runs", "two_symbols"])
+def test_conv_adversarial_inputs(parem, torch_mod, k, kind):
+    """Inputs on which routes do NOT merge to <= 4 states inside a chunk (a repeated symbol
+    keeps the cycle points of one column alive, short periods keep a few states apart):
+    the join composes small maps in parallel instead of walking chunks one by one."""
+    c = synth.config(k, n=1 << 20)
+    rng = np.random.default_rng(k)
+    n = (1 << 21) + 5
+    if kind == "zeros":
+        x = np.zeros(n, np.uint8)
+    elif kind == "period3":
+        x = np.resize(np.array([1, 2, 3], np.uint8), n)
+    elif kind == "two_symbols":
+        x = rng.integers(0, 2, n).astype(np.uint8)
+    else:
+        x = np.repeat(rng.integers(0, c.A, n // 1000 + 1).astype(np.uint8), 1000)[:n]
+    for L in (0, 4096):
+        check(parem, torch_mod, c.table, c.start, c.accept, x, parem.options(chunk_len=L, kernel="conv"))
+    check_find(parem, torch_mod, c.table, c.start, c.accept, x, parem.options(kernel="conv"), cap=1000)
