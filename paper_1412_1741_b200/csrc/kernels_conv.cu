@@ -79,16 +79,20 @@ struct ConvWs {        // the converging path's workspace after the 256-byte hea
     SurvRec* surv;
     EndSet* ends;
     MapRec* maps;
-    BlockMap* bmaps;
-    uint32_t* bin;     // entering index per block (+ the final index at [nblocks])
+    BlockMap* bmaps;   // per block of kBlk chunks
+    BlockMap* smaps;   // per super-block of kBlk blocks
+    uint32_t* bin;     // entering index per block
+    uint32_t* sin;     // entering index per super-block
 };
 
 __host__ __device__ __forceinline__ size_t alw(size_t x) { return (x + 255) & ~(size_t)255; }
 
 __host__ __device__ __forceinline__ size_t conv_ws_bytes(uint64_t p) {
     const uint64_t nb = (p + kBlk - 1) / kBlk;
+    const uint64_t ns = (nb + kBlk - 1) / kBlk;
     return alw(p * sizeof(ConvChunk)) + alw(p * sizeof(SurvRec)) + alw(p * sizeof(EndSet)) +
-           alw(p * sizeof(MapRec)) + alw(nb * sizeof(BlockMap)) + alw(4 * (nb + 1));
+           alw(p * sizeof(MapRec)) + alw(nb * sizeof(BlockMap)) + alw(ns * sizeof(BlockMap)) + alw(4 * (nb + 1)) +
+           alw(4 * (ns + 1));
 }
 
 __device__ __forceinline__ ConvWs conv_ws(const MatchParams& P) {
@@ -99,8 +103,11 @@ __device__ __forceinline__ ConvWs conv_ws(const MatchParams& P) {
     w.surv = reinterpret_cast<SurvRec*>(o); o += alw(p * sizeof(SurvRec));
     w.ends = reinterpret_cast<EndSet*>(o); o += alw(p * sizeof(EndSet));
     w.maps = reinterpret_cast<MapRec*>(o); o += alw(p * sizeof(MapRec));
+    const uint64_t ns = (nb + kBlk - 1) / kBlk;
     w.bmaps = reinterpret_cast<BlockMap*>(o); o += alw(nb * sizeof(BlockMap));
-    w.bin = reinterpret_cast<uint32_t*>(o);
+    w.smaps = reinterpret_cast<BlockMap*>(o); o += alw(ns * sizeof(BlockMap));
+    w.bin = reinterpret_cast<uint32_t*>(o); o += alw(4 * (nb + 1));
+    w.sin = reinterpret_cast<uint32_t*>(o);
     return w;
 }
 
@@ -697,27 +704,53 @@ __global__ void __launch_bounds__(kFollowThreads) conv_block_kernel(const MatchP
     W.bmaps[b].idx[lane] = (uint8_t)idx;
 }
 
-// E4: one warp walks the block maps along q0's path (32 block maps loaded at a time).
+// E3b: compose the block maps of each super-block of kBlk blocks (warp per super-block).
+__global__ void __launch_bounds__(kFollowThreads) conv_super_kernel(const MatchParams P) {
+    const uint64_t sb = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nb = (P.p + kBlk - 1) / kBlk, ns = (nb + kBlk - 1) / kBlk;
+    if (sb >= ns || (P.hdr->err & 2u)) return;
+    const ConvWs W = conv_ws(P);
+    const uint64_t b0 = sb * kBlk, b1 = min(nb, b0 + kBlk);
+    const uint64_t c0 = b0 * kBlk;
+    const uint32_t nin = c0 == 0 ? 1u : W.ends[c0 - 1].n;
+    uint32_t idx = lane < nin ? lane : 0;
+    for (uint64_t b = b0; b < b1; ++b) idx = W.bmaps[b].idx[idx];
+    W.smaps[sb].idx[lane] = (uint8_t)idx;
+}
+
+// E4: one warp walks the super-block maps along q0's path (32 loaded at a time), then
+// E4b resolves the entering index of every block (thread per super-block).
 __global__ void conv_path_kernel(const MatchParams P) {
     const uint32_t lane = threadIdx.x & 31u;
     if (threadIdx.x >= 32 || (P.hdr->err & 2u)) return;
     const ConvWs W = conv_ws(P);
-    const uint64_t nb = (P.p + kBlk - 1) / kBlk;
+    const uint64_t nb = (P.p + kBlk - 1) / kBlk, ns = (nb + kBlk - 1) / kBlk;
     uint32_t e = 0;
-    for (uint64_t b0 = 0; b0 < nb; b0 += 32) {
+    for (uint64_t s0 = 0; s0 < ns; s0 += 32) {
         uint32_t v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = b0 + j < nb ? W.bmaps[b0 + j].idx[lane] : 0u;
+        for (int j = 0; j < 32; ++j) v[j] = s0 + j < ns ? W.smaps[s0 + j].idx[lane] : 0u;
 #pragma unroll
         for (int j = 0; j < 32; ++j)
-            if (b0 + j < nb) {
-                if (lane == 0) W.bin[b0 + j] = e;
+            if (s0 + j < ns) {
+                if (lane == 0) W.sin[s0 + j] = e;
                 e = __shfl_sync(0xFFFFFFFFu, v[j], e);
             }
     }
-    if (lane == 0) {
-        W.bin[nb] = e;
-        P.hdr->final_q = W.ends[P.p - 1].s[e];
+    if (lane == 0) P.hdr->final_q = W.ends[P.p - 1].s[e];
+}
+
+__global__ void __launch_bounds__(kFollowThreads) conv_blockin_kernel(const MatchParams P) {
+    const uint64_t sb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t nb = (P.p + kBlk - 1) / kBlk, ns = (nb + kBlk - 1) / kBlk;
+    if (sb >= ns || (P.hdr->err & 2u)) return;
+    const ConvWs W = conv_ws(P);
+    uint32_t e = W.sin[sb];
+    const uint64_t b0 = sb * kBlk, b1 = min(nb, b0 + kBlk);
+    for (uint64_t b = b0; b < b1; ++b) {
+        W.bin[b] = e;
+        e = W.bmaps[b].idx[e];
     }
 }
 
@@ -866,15 +899,21 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     conv_follow_kernel<SMEM, W32><<<g2, kFollowThreads, tb, s>>>(P);
     prof_after("conv_follow", s);
     conv_ends_kernel<<<g2, kFollowThreads, 0, s>>>(P);
+
     int bpm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, conv_map_kernel<SMEM, W32>, kSetWarps * 32, tb);
     if (bpm < 1) bpm = 1;
     const unsigned gm = (unsigned)(g1w < (uint64_t)sms * bpm ? g1w : (uint64_t)sms * bpm);
     conv_map1_kernel<W32><<<g2, kFollowThreads, 0, s>>>(P);
+
     conv_map_kernel<SMEM, W32><<<gm, kSetWarps * 32, tb, s>>>(P);
+
     const uint64_t nb = (P.p + kBlk - 1) / kBlk;
     conv_block_kernel<<<(unsigned)((nb * 32 + kFollowThreads - 1) / kFollowThreads), kFollowThreads, 0, s>>>(P);
+    const uint64_t nsb = (nb + kBlk - 1) / kBlk;
+    conv_super_kernel<<<(unsigned)((nsb * 32 + kFollowThreads - 1) / kFollowThreads), kFollowThreads, 0, s>>>(P);
     conv_path_kernel<<<1, 32, 0, s>>>(P);
+    conv_blockin_kernel<<<(unsigned)((nsb + kFollowThreads - 1) / kFollowThreads), kFollowThreads, 0, s>>>(P);
     conv_seq_kernel<W32><<<1, 32, 0, s>>>(P);
     prof_after("conv_join", s);
     conv_resolve_kernel<<<(unsigned)((nb + kFollowThreads - 1) / kFollowThreads), kFollowThreads, 0, s>>>(P);
