@@ -104,7 +104,7 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
             const uint64_t target = (uint64_t)sms * bps * kTinyThreads * kTinyRowsPerThread;
             L = ceil_div(n, target);
             L = (L + 63) & ~63ull;       // whole TMA boxes per row
-            if (L < 256) L = 256;
+            if (L < 64) L = 64;   // one TMA box per row: small inputs still spread over many CTAs
         }
         plan->tma = stages;
         if (L > (1ull << 30)) L = 1ull << 30;
