@@ -465,3 +465,61 @@ def test_conv_adversarial_inputs(parem, torch_mod, k, kind):
     for L in (0, 4096):
         check(parem, torch_mod, c.table, c.start, c.accept, x, parem.options(chunk_len=L, kernel="conv"))
     check_find(parem, torch_mod, c.table, c.start, c.accept, x, parem.options(kernel="conv"), cap=1000)
+
+
+# ---------------------------------------------------------------- graphs and streams
+@pytest.mark.parametrize("k", [1, 2, 3, 5])
+def test_graph_capture_replay(parem, torch_mod, k):
+    """parem_match_async is graph-capturable (tiny: one kernel; converging path: eight):
+    a captured match replayed over new contents of the same input buffer stays exact
+    (the clean-workspace contract holds across replays)."""
+    torch = torch_mod
+    c = synth.config(k, n=400_003)
+    with parem.Dfa(c.table, c.start, c.accept) as d:
+        opts = parem.options(ws_clean=True)
+        ws = torch.zeros(d.workspace_bytes(c.n, opts), dtype=torch.uint8, device="cuda")
+        res = torch.zeros(64, dtype=torch.uint8, device="cuda")
+        xd = torch.empty(c.n, dtype=torch.uint8, device="cuda")
+        xd.copy_(torch.from_numpy(c.make_input()))
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            d.match_async(xd, ws, res, opts, s)
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            d.match_async(xd, ws, res, opts, s)
+        rng = np.random.default_rng(k)
+        for rep in range(3):
+            x = c.make_input() if rep == 0 else synth.uniform_symbols(c.n, c.A, seed=100 + rep)
+            xd.copy_(torch.from_numpy(x))
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            got = parem.MatchResult.from_bytes(res.cpu().numpy().tobytes()[:56])
+            ref = oracle.walk(c.table, c.start, c.accept, x)
+            assert (got.final_state, got.accepted, got.match_count) == (ref.final_state, ref.accepted, ref.match_count)
+
+
+def test_concurrent_streams(parem, torch_mod):
+    """One immutable DFA handle, two streams, two workspaces, different inputs in flight."""
+    torch = torch_mod
+    c = synth.config(3, n=1_000_003)
+    xa, xb = c.make_input(), synth.uniform_symbols(c.n, c.A, seed=77)
+    ra, rb = (oracle.walk(c.table, c.start, c.accept, x) for x in (xa, xb))
+    with parem.Dfa(c.table, c.start, c.accept) as d:
+        outs = []
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        for x, s in zip((xa, xb), streams):
+            ws = torch.zeros(d.workspace_bytes(c.n), dtype=torch.uint8, device="cuda")
+            res = torch.zeros(64, dtype=torch.uint8, device="cuda")
+            xd = to_dev(torch, x)
+            torch.cuda.synchronize()
+            outs.append((ws, res, xd))
+        for i in range(4):
+            for (ws, res, xd), s in zip(outs, streams):
+                d.match_async(xd, ws, res, None, s)
+        torch.cuda.synchronize()
+        for (ws, res, xd), ref in zip(outs, (ra, rb)):
+            got = parem.MatchResult.from_bytes(res.cpu().numpy().tobytes()[:56])
+            assert (got.final_state, got.accepted, got.match_count) == (ref.final_state, ref.accepted, ref.match_count)
