@@ -52,6 +52,8 @@ def lib():
         L.oracle_walk.argtypes = [u32, u32, p, u32, u32, p, p, u64, C.POINTER(_Res)]
         L.oracle_states_at.restype = C.c_int
         L.oracle_states_at.argtypes = [u32, u32, p, u32, u32, p, u64, p, u64, p]
+        L.oracle_lookback_stats.restype = C.c_int
+        L.oracle_lookback_stats.argtypes = [u32, u32, p, u32, p, u64, p, u64, u64, C.POINTER(u64), C.POINTER(u64), p]
         L.oracle_positions.restype = C.c_int
         L.oracle_positions.argtypes = [u32, u32, p, u32, u32, p, p, u64, p, u64, C.POINTER(u64)]
         L.oracle_route_stats.restype = C.c_int
@@ -137,6 +139,21 @@ def route_stats(table, text, boundaries) -> tuple[int, int]:
                                   b.ctypes.data, b.size - 1, C.byref(r), C.byref(s), scratch.ctypes.data)
     if rc != OK:
         raise ValueError(f"oracle_route_stats failed ({rc})")
+    return r.value, s.value
+
+
+def lookback_stats(table, text, boundaries, k: int) -> tuple[int, int]:
+    """(routes, route_steps) of the k-symbol look-back rule R_i = delta*(Q, T[b_i-k, b_i)) n S(T[b_i])."""
+    t = _tab(table)
+    Q, A = t.shape
+    T = _bytes(text)
+    b = np.ascontiguousarray(np.asarray(boundaries, dtype=np.uint64))
+    scratch = np.empty(2 * Q, dtype=np.uint8)
+    r, s = C.c_uint64(), C.c_uint64()
+    rc = lib().oracle_lookback_stats(Q, A, t.ctypes.data, t.itemsize, T.ctypes.data, T.size, b.ctypes.data,
+                                     b.size - 1, k, C.byref(r), C.byref(s), scratch.ctypes.data)
+    if rc != OK:
+        raise ValueError(f"oracle_lookback_stats failed ({rc})")
     return r.value, s.value
 
 

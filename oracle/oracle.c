@@ -81,6 +81,45 @@ int oracle_walk(uint32_t Q, uint32_t A, const void* table, uint32_t eb, uint32_t
     return ORACLE_OK;
 }
 
+/* NEXT-2 (i): the k-symbol look-back candidate rule, a generalisation of L (
+ * related work P:529): for i >= 1
+ *   R_i^(k) = delta*(Q, T[max(0, b_i - k), b_i)) n S(T[b_i]),
+ * the states some start can be in after the k symbols before the boundary (DEAD removed),
+ * restricted to those with a transition on the chunk's first symbol; k = 1 is the paper's
+ * R = S n L.  |R_0| = 1.  Direct set iteration, O(p * k * Q). */
+int oracle_lookback_stats(uint32_t Q, uint32_t A, const void* table, uint32_t eb, const uint8_t* T, uint64_t n,
+                          const uint64_t* b, uint64_t p, uint64_t k, uint64_t* routes, uint64_t* route_steps,
+                          uint8_t* scratch /* 2 Q bytes */) {
+    if (p == 0 || b[0] != 0 || b[p] != n || k == 0) return ORACLE_EINVAL;
+    uint8_t* cur = scratch;
+    uint8_t* nxt = scratch + Q;
+    uint64_t r_total = 1, steps = b[1] - b[0];
+    for (uint64_t i = 1; i < p; ++i) {
+        if (b[i] <= b[i - 1] || b[i] >= n) return ORACLE_EINVAL;
+        for (uint32_t q = 0; q < Q; ++q) cur[q] = 1;   /* all of Q */
+        const uint64_t a = b[i] > k ? b[i] - k : 0;
+        for (uint64_t j = a; j < b[i]; ++j) {           /* the image under T[j] */
+            if (T[j] >= A) return ORACLE_ESYMBOL;
+            for (uint32_t q = 0; q < Q; ++q) nxt[q] = 0;
+            for (uint32_t q = 0; q < Q; ++q)
+                if (cur[q]) {
+                    uint32_t d = delta(table, eb, A, q, T[j]);
+                    if (d != ORACLE_DEAD) nxt[d] = 1;
+                }
+            uint8_t* t = cur; cur = nxt; nxt = t;
+        }
+        if (T[b[i]] >= A) return ORACLE_ESYMBOL;
+        uint64_t r = 0;
+        for (uint32_t q = 0; q < Q; ++q)
+            if (cur[q] && delta(table, eb, A, q, T[b[i]]) != ORACLE_DEAD) ++r;
+        r_total += r;
+        steps += r * (b[i + 1] - b[i]);
+    }
+    *routes = r_total;
+    *route_steps = steps;
+    return ORACLE_OK;
+}
+
 /* Match end positions (NEXT-4; Alg. 1's visited-state vector Rr, reduced to the
  * steps whose destination is in F): every k in [0, n) with q_{k+1} in F, ascending, i.e.
  * the 0-based offset of the symbol that completes an occurrence.  Writes min(count, cap)

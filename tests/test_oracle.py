@@ -207,3 +207,42 @@ def test_positions_abb_regex_and_caps():
     assert got.tolist() == [0, 1, 2, 3, 4] and cnt == 5
     got, cnt = oracle.positions(tp, 0, accp, np.array([0, 0, 1], np.uint8))   # dies at offset 1
     assert got.tolist() == [0] and cnt == 1
+
+
+# ---------------------------------------------------------------- NEXT-2 (i): k-symbol look-back
+def test_lookback_k1_is_the_papers_rule():
+    """k = 1: delta*(Q, T[b-1]) n S(T[b]) = L(c_last) n S(c_first), the paper's R (P:67);
+    checked against the independent oracle_route_stats on complete and partial tables."""
+    rng = np.random.default_rng(21)
+    for seed in range(8):
+        Q, A = int(rng.choice([3, 9, 40])), int(rng.choice([2, 4, 26]))
+        t = synth.partial_dfa(Q, A, 0.2, seed, np.uint16) if seed % 2 else synth.random_dfa(Q, A, seed, np.uint16)
+        x = rng.integers(0, A, 5000).astype(np.uint8)
+        b = oracle.grid_boundaries(x.size, int(rng.choice([7, 100, 999])))
+        assert oracle.lookback_stats(t, x, b, 1) == oracle.route_stats(t, x, b)
+
+
+def test_lookback_brute_force_monotone_and_sound():
+    """Python set iteration on tiny DFAs; |R^(k)| never grows with k; the true boundary
+    state is always a candidate (soundness)."""
+    rng = np.random.default_rng(5)
+    for seed in range(6):
+        Q, A = 6, 3
+        t = synth.random_dfa(Q, A, seed, np.uint16).reshape(Q, A)
+        x = rng.integers(0, A, 400).astype(np.uint8)
+        b = oracle.grid_boundaries(x.size, 37)
+        true = oracle.states_at(t, 0, x, b[1:-1])
+        prev = None
+        for k in (1, 2, 3, 5, 50):
+            routes, steps = oracle.lookback_stats(t, x, b, k)
+            want_r, want_s = 1, b[1] - b[0]
+            for i in range(1, len(b) - 1):
+                S = set(range(Q))
+                for j in range(max(0, b[i] - k), b[i]):
+                    S = {int(t[s, x[j]]) for s in S}
+                assert int(true[i - 1]) in S
+                want_r += len(S)
+                want_s += len(S) * (b[i + 1] - b[i])
+            assert (routes, steps) == (want_r, want_s)
+            assert prev is None or routes <= prev
+            prev = routes
