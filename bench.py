@@ -207,7 +207,8 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--boundary", default="auto", choices=["auto", "snap", "grid"])
-    ap.add_argument("--candidates", default="parem", choices=["parem", "enum"])
+    ap.add_argument("--candidates", default="parem", choices=["parem", "enum", "lookback"])
+    ap.add_argument("--lookback", type=int, default=4, help="k for --candidates lookback (NEXT-2 (i))")
     ap.add_argument("--chunk-len", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -246,7 +247,8 @@ def main():
     dfa = P.Dfa(cfg.table, cfg.start, cfg.accept)
     # the workspace starts zero-filled and every completed match leaves it so: no per-call
     # header reset, a step is exactly the path's kernel launches
-    opts = P.options(chunk_len=args.chunk_len, boundary=args.boundary, candidates=args.candidates, ws_clean=True)
+    opts = P.options(chunk_len=args.chunk_len, boundary=args.boundary, candidates=args.candidates, ws_clean=True,
+                     lookback=args.lookback if args.candidates == "lookback" else 0)
     plan = dfa.plan(n, opts)
     info = dfa.info()
     wsb = torch.zeros(dfa.workspace_bytes(n, opts), dtype=torch.uint8, device=f"cuda:{local}")
@@ -434,7 +436,8 @@ def main():
         "data": "synthetic (seeded, SURVEY §8(d) recipe; no public dataset in the paper)",
         "config": {"workload": f"cfg{cfg.index}: {cfg.name}", "n_bytes": n, "states": cfg.Q, "alphabet": cfg.A,
                    "boundary": {0: "grid", 1: "snap"}.get(plan["boundary_policy"], args.boundary),
-                   "candidates": args.candidates, "kernel": plan["kernel"],
+                   "candidates": args.candidates + (f" k={args.lookback}" if args.candidates == "lookback" else ""),
+                   "kernel": plan["kernel"],
                    "chunks": plan["num_chunks"], "chunk_len": plan["chunk_len"], "grid": plan["grid_blocks"],
                    "block": plan["block_threads"], "slots": plan["slots"],
                    "l2": "input larger than L2 (no flush needed)" if n > (126 << 20) else "input fits L2 (warm)",

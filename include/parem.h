@@ -57,6 +57,8 @@ extern "C" {
 /* candidates */
 #define PAREM_CANDIDATES_PAREM 0u  /* R_i = S n L (the paper's rule)                        */
 #define PAREM_CANDIDATES_ENUM 1u   /* every chunk i >= 1 starts from all of Q (Enum) */
+#define PAREM_CANDIDATES_LOOKBACK 2u /* R_i = delta*(Q, T[b_i - k, b_i)) n S(T[b_i]), k = options.lookback
+                                        (NEXT-2 (i); k = 1 is the paper's rule); tiny kernel only */
 
 /* Result of one match (56 bytes).  routes = sum_i |R_i| ("calculations"; with
  * |R_0| = 1), route_steps = sum_i |R_i| * len_i (candidate-steps, the lookup roofline's
@@ -83,7 +85,8 @@ typedef struct parem_options {
     uint32_t candidates;
     uint32_t kernel;       /* 0 = auto; 1 = tiny (thread per chunk); 2 = lanes (group per chunk); 3 = conv (converging: set walk + follow + join) */
     uint32_t flags;        /* PAREM_FLAG_* */
-    uint32_t reserved[2];
+    uint32_t lookback;     /* k for PAREM_CANDIDATES_LOOKBACK (>= 1) */
+    uint32_t reserved;
 } parem_options;
 
 /* flags: the workspace's 64-byte header is already zero -- freshly zero-filled by the

@@ -56,12 +56,12 @@ class MatchResult(NamedTuple):
 
 
 _POLICY = {"grid": BOUNDARY_GRID, "snap": BOUNDARY_SNAP, "auto": BOUNDARY_AUTO}
-_CAND = {"parem": CANDIDATES_PAREM, "enum": CANDIDATES_ENUM}
+_CAND = {"parem": CANDIDATES_PAREM, "enum": CANDIDATES_ENUM, "lookback": _abi.CANDIDATES_LOOKBACK}
 _KERNEL = {"auto": KERNEL_AUTO, "tiny": KERNEL_TINY, "lanes": KERNEL_LANES, "conv": KERNEL_CONV}
 
 
 def options(chunk_len: int = 0, boundary: str = "auto", candidates: str = "parem", kernel: str = "auto",
-            ws_clean: bool = False):
+            ws_clean: bool = False, lookback: int = 0):
     """parem_options.  ``ws_clean`` sets PAREM_FLAG_WS_CLEAN: the workspace header is known
     to be zero (torch.zeros, or a previous completed call), so no per-call reset is issued."""
     o = _abi.parem_options()
@@ -70,6 +70,7 @@ def options(chunk_len: int = 0, boundary: str = "auto", candidates: str = "parem
     o.candidates = _CAND[candidates]
     o.kernel = _KERNEL[kernel]
     o.flags = _abi.FLAG_WS_CLEAN if ws_clean else 0
+    o.lookback = int(lookback)
     return o
 
 

@@ -10,7 +10,7 @@ SO_PATH = os.environ.get("PAREM_LIB") or os.path.join(_HERE, "libparem.so")
 PAREM_OK, PAREM_EINVAL, PAREM_ESYMBOL, PAREM_ECUDA, PAREM_ENOMEM, PAREM_EINTERNAL = 0, -1, -2, -3, -4, -5
 PAREM_DEAD = 0xFFFFFFFF
 BOUNDARY_GRID, BOUNDARY_SNAP, BOUNDARY_AUTO = 0, 1, 2
-CANDIDATES_PAREM, CANDIDATES_ENUM = 0, 1
+CANDIDATES_PAREM, CANDIDATES_ENUM, CANDIDATES_LOOKBACK = 0, 1, 2
 KERNEL_AUTO, KERNEL_TINY, KERNEL_LANES, KERNEL_CONV = 0, 1, 2, 3
 
 
@@ -22,7 +22,7 @@ class parem_result(C.Structure):
 
 class parem_options(C.Structure):
     _fields_ = [("chunk_len", C.c_uint64), ("boundary_policy", C.c_uint32), ("candidates", C.c_uint32),
-                ("kernel", C.c_uint32), ("flags", C.c_uint32), ("reserved", C.c_uint32 * 2)]
+                ("kernel", C.c_uint32), ("flags", C.c_uint32), ("lookback", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 FLAG_WS_CLEAN = 1

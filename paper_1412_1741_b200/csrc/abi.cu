@@ -118,6 +118,7 @@ static int match_impl(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, 
     P.slots = plan.slots;
     P.tg = plan.tg;
     P.dmax = plan.dmax;
+    P.lookback = opts ? opts->lookback : 0;
     P.offset_base = offset_base;
     P.carry = d_carry;
     P.result = d_result;

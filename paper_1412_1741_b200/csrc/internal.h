@@ -67,6 +67,7 @@ struct MatchParams {
     uint32_t tg;               // lanes: threads per chunk group
     uint32_t stages;           // tiny: TMA stages per warp (0 = no TMA)
     uint32_t dmax;             // conv: survivors handed from the set walk to the follow walk
+    uint32_t lookback;         // tiny: k of the look-back candidate rule
     uint64_t offset_base;
     const parem_result* carry; // may be null
     parem_result* result;

@@ -193,21 +193,52 @@ struct Routes {
     }
 };
 
-// One chunk's A2 data: boundaries [b0, b1), candidate list R_i (Llist[loff .. loff + cnt)),
-// q0 for chunk 0, and |R_i| for the stats (rc).
+// One chunk's A2 data: boundaries [b0, b1), candidate list R_i (Llist[loff .. loff + cnt),
+// or -- look-back rule -- the set bits of `mask`), q0 for chunk 0, and |R_i| for the stats.
 struct TinyChunk {
     uint64_t t, b0, b1;
-    uint32_t cnt, loff, q0, rc;
+    uint32_t cnt, loff, q0, rc, mask;
     bool live;
 };
 
+// j-th candidate start state of chunk c
+__device__ __forceinline__ uint32_t tiny_cand(const TinyChunk& c, const uint32_t* Llist, uint32_t j) {
+    return c.mask ? (uint32_t)__fns(c.mask, 0, (int)j + 1) : Llist[c.loff + j];
+}
+
 __device__ __forceinline__ TinyChunk tiny_chunk(const MatchParams& P, uint64_t t, const uint32_t* Lcnt,
-                                                const uint32_t* Loff) {
+                                                const uint32_t* Loff, const uint16_t* tab1) {
     TinyChunk c;
     c.t = t;
     c.live = t < P.p;
     c.b0 = c.b1 = 0;
-    c.cnt = c.loff = c.q0 = c.rc = 0;
+    c.cnt = c.loff = c.q0 = c.rc = c.mask = 0;
+    if (c.live && t > 0 && P.cand == PAREM_CANDIDATES_LOOKBACK) {
+        // NEXT-2 (i): R = delta*(Q, T[b0 - k, b0)) n S(T[b0]) as a bit set over <= 32 states
+        // (the sink of a partial table is DEAD, never a candidate: C9/C10)
+        const DevDfa& d = P.d;
+        c.b0 = boundary_of(P, t, Lcnt);
+        c.b1 = boundary_of(P, t + 1, Lcnt);
+        const uint32_t nosink = d.has_sink ? ~(1u << d.sink) : ~0u;
+        uint32_t m = (d.Qp >= 32 ? ~0u : (1u << d.Qp) - 1u) & nosink;
+        for (uint64_t j = c.b0 > P.lookback ? c.b0 - P.lookback : 0; j < c.b0; ++j) {
+            uint32_t ch = P.in[j];
+            if (ch >= d.A) ch = d.A - 1;   // ESYMBOL is reported anyway; keep the set valid
+            uint32_t nm = 0;
+            for (uint32_t r = m; r; r &= r - 1) nm |= 1u << (tab1[(__ffs(r) - 1) * d.A + ch] & 0x7FFFu);
+            m = nm & nosink;
+        }
+        c.mask = m ? m : 0u;
+        c.cnt = __popc(m);
+        uint32_t cf = P.in[c.b0];
+        if (cf >= d.A) cf = d.A - 1;
+        uint32_t inS = 0;   // |R n S(c_first)|
+        for (uint32_t r = m; r; r &= r - 1)
+            inS += !d.has_sink || (tab1[(__ffs(r) - 1) * d.A + cf] & 0x7FFFu) != d.sink;
+        c.rc = inS;
+        if (!m) c.cnt = 0;
+        return c;
+    }
     if (c.live) {
         c.b0 = boundary_of(P, t, Lcnt);
         c.b1 = boundary_of(P, t + 1, Lcnt);
@@ -276,8 +307,8 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
     __syncthreads();
 
     // ---- A2: this lane's two chunks (rows lane and lane + 32 of the warp's box) and R_i ----
-    const TinyChunk ca = tiny_chunk(P, row0 + lane, Lcnt, Loff);
-    const TinyChunk cb = tiny_chunk(P, row0 + 32 + lane, Lcnt, Loff);
+    const TinyChunk ca = tiny_chunk(P, row0 + lane, Lcnt, Loff, tab1);
+    const TinyChunk cb = tiny_chunk(P, row0 + 32 + lane, Lcnt, Loff, tab1);
     const bool act_a = ca.live && ca.cnt, act_b = cb.live && cb.cnt;
     // per-byte invalid bits for A = 1, 2, 4 (powers of two): every bit at or above log2(A)
     const uint32_t bm = B ? (0xFFu & ~(A - 1u)) * 0x01010101u : 0u;
@@ -293,8 +324,8 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
     for (int j = 0; j < K; ++j) {
         const uint32_t ka = ca.cnt ? min((uint32_t)j, ca.cnt - 1) : 0;
         const uint32_t kb = cb.cnt ? min((uint32_t)j, cb.cnt - 1) : 0;
-        const uint32_t sa = ca.t == 0 ? ca.q0 : (ca.cnt ? Llist[ca.loff + ka] : 0u);
-        const uint32_t sb = cb.cnt ? Llist[cb.loff + kb] : 0u;
+        const uint32_t sa = ca.t == 0 ? ca.q0 : (ca.cnt ? tiny_cand(ca, Llist, ka) : 0u);
+        const uint32_t sb = cb.cnt ? tiny_cand(cb, Llist, kb) : 0u;
         ra.e[j] = B ? ((sa << 11) | lane4) : sa;
         rb.e[j] = B ? ((sb << 11) | lane4) : sb;
         ra.h[j] = rb.h[j] = 0;
@@ -418,7 +449,7 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
 #pragma unroll
         for (int j = 0; j < K; ++j)
             if ((uint32_t)j < c.cnt) {
-                const uint32_t s = c.t == 0 ? c.q0 : Llist[c.loff + j];
+                const uint32_t s = c.t == 0 ? c.q0 : tiny_cand(c, Llist, j);
                 mend[lr * Qpad + s] = (uint8_t)r.state(j);
                 mhits[lr * Qpad + s] = r.h[j];
             }
@@ -429,7 +460,7 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
             x.m16 = r.m16;
 #pragma unroll
             for (int j = 0; j < K; ++j) {
-                const uint32_t s = Llist[c.loff + min(base + (uint32_t)j, c.cnt - 1)];
+                const uint32_t s = tiny_cand(c, Llist, min(base + (uint32_t)j, c.cnt - 1));
                 x.e[j] = B ? ((s << 11) | lane4) : s;
                 x.h[j] = 0;
             }
@@ -437,7 +468,7 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
 #pragma unroll
             for (int j = 0; j < K; ++j)
                 if (base + (uint32_t)j < c.cnt) {
-                    const uint32_t s = Llist[c.loff + base + j];
+                    const uint32_t s = tiny_cand(c, Llist, base + j);
                     mend[lr * Qpad + s] = (uint8_t)x.state(j);
                     mhits[lr * Qpad + s] = x.h[j];
                 }

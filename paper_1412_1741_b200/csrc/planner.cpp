@@ -49,7 +49,11 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
     const uint32_t kreq = opts ? opts->kernel : 0;
     const uint64_t forced = opts ? opts->chunk_len : 0;
     if (policy > PAREM_BOUNDARY_AUTO) { set_error("bad boundary_policy %u", policy); return PAREM_EINVAL; }
-    if (cand > PAREM_CANDIDATES_ENUM) { set_error("bad candidates %u", cand); return PAREM_EINVAL; }
+    if (cand > PAREM_CANDIDATES_LOOKBACK) { set_error("bad candidates %u", cand); return PAREM_EINVAL; }
+    if (cand == PAREM_CANDIDATES_LOOKBACK && (!opts || opts->lookback == 0)) {
+        set_error("look-back candidates need options.lookback >= 1");
+        return PAREM_EINVAL;
+    }
     if (kreq > kKernelConv) { set_error("bad kernel %u", kreq); return PAREM_EINVAL; }
     plan->cand = cand;
     if (n == 0) {
@@ -72,6 +76,10 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         set_error("converging path needs a complete table of <= 65536 states whose routes merge");
         return PAREM_EINVAL;
     }
+    if (cand == PAREM_CANDIDATES_LOOKBACK && kernel != kKernelTiny) {
+        set_error("look-back candidates are implemented by the tiny kernel (<= %u states)", kTinyMaxStates);
+        return PAREM_EINVAL;
+    }
     if (kernel == kKernelTiny && d.Qp > kTinyMaxStates) {
         set_error("tiny kernel needs <= %u internal states (have %u)", kTinyMaxStates, d.Qp);
         return PAREM_EINVAL;
@@ -91,7 +99,11 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
 
     if (kernel == kKernelTiny) {
         const uint32_t B = d.sym_bits;
-        uint32_t need = cand == PAREM_CANDIDATES_ENUM ? d.Q : (policy == PAREM_BOUNDARY_SNAP ? d.Lmin : d.Lmax);
+        // look-back sets are at most |L(c)|; from k >= 4 on usually far smaller (size for the
+        // smallest |L(c)|, extra passes cover the rest)
+        const bool lb_small = cand == PAREM_CANDIDATES_LOOKBACK && opts->lookback >= 4;
+        uint32_t need = cand == PAREM_CANDIDATES_ENUM ? d.Q
+                        : (lb_small || policy == PAREM_BOUNDARY_SNAP) ? d.Lmin : d.Lmax;
         if (need < 1) need = 1;
         const uint32_t K = tiny_round_slots(need, B);
         const uint32_t stages = (forced == 0 || forced % 64 == 0) ? tiny_pick_stages(d, B) : 0u;

@@ -523,3 +523,40 @@ def test_concurrent_streams(parem, torch_mod):
         for (ws, res, xd), ref in zip(outs, (ra, rb)):
             got = parem.MatchResult.from_bytes(res.cpu().numpy().tobytes()[:56])
             assert (got.final_state, got.accepted, got.match_count) == (ref.final_state, ref.accepted, ref.match_count)
+
+
+# ---------------------------------------------------------------- NEXT-2 (i): look-back candidates
+@pytest.mark.parametrize("k_lb", [1, 2, 4, 16])
+def test_lookback_candidates(parem, torch_mod, k_lb):
+    """R_i = delta*(Q, T[b_i - k, b_i)) n S(T[b_i]) in the tiny kernel: results exact, and the
+    GPU's routes / route_steps equal the oracle's look-back statistics (k = 1: the paper's)."""
+    rng = np.random.default_rng(k_lb)
+    cases = [(synth.config(1, n=200_003), None), (synth.config(2, n=300_001), None)]
+    for k, cfg in enumerate(cases):
+        c = cfg[0]
+        x = c.make_input()
+        for L in (64, 1000):
+            got = check(parem, torch_mod, c.table, c.start, c.accept, x,
+                        parem.options(chunk_len=L, boundary="grid", candidates="lookback", lookback=k_lb))
+            b = oracle.grid_boundaries(x.size, L)
+            assert (got.routes, got.route_steps) == oracle.lookback_stats(c.table, x, b, k_lb)
+            if k_lb == 1:
+                assert (got.routes, got.route_steps) == oracle.route_stats(c.table, x, b)
+    for seed in range(6):
+        Q, A = int(rng.choice([3, 9, 20, 31])), int(rng.choice([2, 4, 7]))
+        t = synth.partial_dfa(Q, A, 0.1, seed, np.uint16) if seed % 2 else synth.random_dfa(Q, A, seed, np.uint16)
+        acc = rng.random(Q) < 0.3
+        x = rng.integers(0, A, 50_000).astype(np.uint8)
+        got = check(parem, torch_mod, t, 0, acc, x, parem.options(chunk_len=97, boundary="grid",
+                                                                 candidates="lookback", lookback=k_lb))
+        assert (got.routes, got.route_steps) == oracle.lookback_stats(t, x, oracle.grid_boundaries(x.size, 97), k_lb)
+        check(parem, torch_mod, t, 0, acc, x, parem.options(candidates="lookback", lookback=k_lb))   # planner + SNAP/AUTO
+
+
+def test_lookback_rejected_off_tiny(parem, torch_mod):
+    c = synth.config(3, n=1000)
+    with parem.Dfa(c.table, c.start, c.accept) as d:
+        with pytest.raises(parem.ParemError):
+            d.match(to_dev(torch_mod, c.make_input()), parem.options(candidates="lookback", lookback=4))
+        with pytest.raises(parem.ParemError):
+            d.match(to_dev(torch_mod, c.make_input()), parem.options(candidates="lookback"))
