@@ -17,8 +17,9 @@
 //   E1..E5          the join as a composition of small maps: each chunk's end set (<= 32
 //                   states, 1 once its routes merged), each chunk as a map from the previous
 //                   end set (head walks, lanes of a warp), block composition, one warp along
-//                   q0's path, per-chunk resolution and the result.  Only wide chunks fall
-//                   back to one sequential thread.
+//                   q0's path, per-chunk resolution and the result.  Wide chunks are
+//                   resolved by one warp in chunk order (whole-chunk walks from their
+//                   entering set), the rest in parallel.
 // Every input byte is validated once (reading C11): K2 tails, E2 heads and open tails.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -541,7 +542,7 @@ __device__ __forceinline__ uint32_t walk1(const DevDfa& d, const uint8_t* in, ui
 // entering index), E4 walks the block maps along q0's path, E5 resolves every chunk's
 // entering state and hits in parallel and writes the result.  Every step is parallel
 // whether or not routes merged; only "wide" chunks (the set never shrank to 32 states)
-// fall back to one sequential thread (conv_seq_kernel).
+// are resolved by one warp in chunk order (conv_wide_kernel), each from its entering set.
 
 // E1: end set of every chunk (distinct survivor ends) and each survivor's index in it.
 __global__ void __launch_bounds__(kFollowThreads) conv_ends_kernel(const MatchParams P) {
@@ -550,9 +551,9 @@ __global__ void __launch_bounds__(kFollowThreads) conv_ends_kernel(const MatchPa
     const ConvWs W = conv_ws(P);
     SurvRec& s = W.surv[t];
     EndSet& es = W.ends[t];
-    if (W.info[t].D == kWide) {
+    if (W.info[t].D == kWide) {   // resolved by conv_wide_kernel from its entering set
         es.n = 0;
-        atomicOr(&P.hdr->err, 2u);
+        atomicOr(&P.hdr->err, 4u);
         return;
     }
     uint32_t n = 0;
@@ -564,6 +565,87 @@ __global__ void __launch_bounds__(kFollowThreads) conv_ends_kernel(const MatchPa
         s.eidx[k] = (uint8_t)j;
     }
     es.n = n;
+}
+
+// E1b: "wide" chunks (their set walk never shrank to 32 states), in chunk order, by one
+// warp: lane j walks the WHOLE chunk from state j of the previous chunk's end set (<= 32;
+// a wide predecessor was resolved just before), the distinct end states become this
+// chunk's end set and its map is written directly.  Runs only if a wide chunk exists;
+// every other chunk stays on the parallel path.
+template <bool W32>
+__global__ void conv_wide_kernel(const MatchParams P) {
+    if (threadIdx.x >= 32 || !(P.hdr->err & 4u)) return;
+    const uint32_t lane = threadIdx.x;
+    const ConvWs W = conv_ws(P);
+    const DevDfa& d = P.d;
+    Tab<false, W32> T;
+    T.init(d, 0u);
+    const uint8_t* in = P.in;
+    unsigned long long routes = 0, steps = 0;
+    for (uint64_t t0 = 0; t0 < P.p; t0 += 32) {
+        const bool w = t0 + lane < P.p && W.info[t0 + lane].D == kWide;
+        uint32_t wide = __ballot_sync(0xFFFFFFFFu, w);
+        while (wide) {
+            const uint64_t t = t0 + (uint64_t)(__ffs(wide) - 1);
+            wide &= wide - 1;
+            const uint64_t b0 = conv_b(P, t), b1 = conv_b(P, t + 1);
+            bool dead;
+            const uint32_t nin = t == 0 ? 1u : W.ends[t - 1].n;
+            const uint32_t q = t == 0 ? start_state(P, &dead) : W.ends[t - 1].s[lane < nin ? lane : 0];
+            uint32_t e = q * T.ES, h = 0;
+            bool badseen = false;
+            for (uint64_t pos = b0; pos < b1; pos += 32) {
+                const uint32_t cnt = (uint32_t)min((uint64_t)32, b1 - pos);
+                const uint32_t mine = lane < cnt ? (uint32_t)__ldg(in + pos + lane) : 0u;
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, lane < cnt && mine >= d.A);
+                if (bal && !badseen) {
+                    badseen = true;
+                    if (lane == 0) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)(pos + __ffs(bal) - 1));
+                }
+                for (uint32_t k = 0; k < cnt; ++k) {
+                    e = T.next(e, T.col(__shfl_sync(0xFFFFFFFFu, mine, k)));
+                    h += T.hit(e);
+                }
+            }
+            // distinct ends of the valid lanes -> this chunk's end set (lane order); every
+            // lane takes part in every collective
+            const uint32_t e0 = __shfl_sync(0xFFFFFFFFu, e, 0);
+            const uint32_t z = lane < nin ? T.state(e) : T.state(e0);
+            const uint32_t valid = nin >= 32 ? 0xFFFFFFFFu : ((1u << nin) - 1u);
+            const uint32_t m = __match_any_sync(0xFFFFFFFFu, z) & valid;
+            const uint32_t first = m ? (uint32_t)(__ffs(m) - 1) : 0u;   // leader of my class
+            const uint32_t leaders = __ballot_sync(0xFFFFFFFFu, lane < nin && first == lane);
+            const uint32_t idx = __popc(leaders & ((1u << first) - 1u));
+            if ((leaders >> lane) & 1u) {
+                W.ends[t].s[idx] = z;
+                W.surv[t].z[idx] = z;
+                W.surv[t].end[idx] = z;
+                W.surv[t].tail[idx] = 0;
+                W.surv[t].eidx[idx] = (uint8_t)idx;
+            }
+            if (lane < nin) {
+                W.maps[t].idx[lane] = (uint8_t)idx;
+                W.maps[t].hits[lane] = h;
+            }
+            if (lane == 0) {
+                W.ends[t].n = __popc(leaders);
+                W.surv[t].n = __popc(leaders);
+                uint64_t rc = 1;
+                if (t > 0) {
+                    const uint32_t cl = in[b0 - 1];
+                    const uint32_t li = (P.cand == PAREM_CANDIDATES_ENUM || cl >= d.A) ? d.A : cl;
+                    rc = route_count(P, cl, in[b0], __ldg(d.Lcnt + li));
+                }
+                routes += rc;
+                steps += rc * (b1 - b0);
+            }
+            __syncwarp();
+        }
+    }
+    if (lane == 0 && routes) {
+        atomicAdd(&P.hdr->routes, routes);
+        atomicAdd(&P.hdr->steps, steps);
+    }
 }
 
 // E2a: chunks entered from ONE possible state (chunk 0, or the previous chunk's routes all
@@ -578,7 +660,7 @@ __global__ void __launch_bounds__(kFollowThreads) conv_map1_kernel(const MatchPa
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t A = d.A;
     unsigned long long rc = 0, steps = 0;
-    if (t < P.p && !(P.hdr->err & 2u) && (t == 0 || W.ends[t - 1].n == 1)) {
+    if (t < P.p && !(P.hdr->err & 2u) && W.info[t].D != kWide && (t == 0 || W.ends[t - 1].n == 1)) {
         const uint64_t b0 = conv_b(P, t), b1 = conv_b(P, t + 1);
         const ConvChunk& c = W.info[t];
         const SurvRec& s = W.surv[t];
@@ -635,7 +717,7 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_map_kernel(const MatchPar
     const bool skip = (P.hdr->err & 2u) != 0;   // wide chunks: the sequential fallback resolves
     unsigned long long routes = 0, steps = 0;
     for (uint64_t t = (uint64_t)blockIdx.x * kSetWarps + warp; t < P.p && !skip; t += (uint64_t)gridDim.x * kSetWarps) {
-        if (t == 0) continue;
+        if (t == 0 || W.info[t].D == kWide) continue;   // wide: conv_wide_kernel's
         const uint32_t nin = W.ends[t - 1].n;
         if (nin <= 1) continue;   // conv_map1_kernel's
         const uint64_t b0 = conv_b(P, t), b1 = conv_b(P, t + 1);
@@ -754,65 +836,6 @@ __global__ void __launch_bounds__(kFollowThreads) conv_blockin_kernel(const Matc
     }
 }
 
-// Walk one route from state q over in[a, b) (global table); hits optional.
-template <bool W32>
-__device__ uint32_t walk_seq(const DevDfa& d, const uint8_t* in, uint64_t a, uint64_t b, uint32_t q, uint32_t* hits) {
-    return walk1<W32>(d, in, a, b, q, hits);
-}
-
-// Sequential fallback, only when a wide chunk exists: resolve every chunk on one thread.
-template <bool W32>
-__global__ void conv_seq_kernel(const MatchParams P) {
-    if (threadIdx.x != 0 || !(P.hdr->err & 2u)) return;
-    const ConvWs W = conv_ws(P);
-    const DevDfa& d = P.d;
-    bool dead;
-    uint32_t q = start_state(P, &dead);
-    unsigned long long hits = 0, routes = 0, steps = 0;
-    for (uint64_t i = 0; i < P.p; ++i) {
-        const uint64_t b0 = conv_b(P, i), b1 = conv_b(P, i + 1);
-        const ConvChunk& c = W.info[i];
-        uint32_t h = 0, nq;
-        if (c.D == kWide) {
-            nq = walk_seq<W32>(d, P.in, b0, b1, q, &h);
-            const uint64_t off = first_bad(P.in, b0, b1, d.A);
-            if (off < b1) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
-        } else {
-            const SurvRec& s = W.surv[i];
-            const uint32_t z = walk_seq<W32>(d, P.in, b0, b0 + c.m, q, &h);
-            uint32_t k = 0;
-            while (k < s.n && s.z[k] != z) ++k;
-            if (k == s.n) {
-                atomicOr(&P.hdr->err, 1u);
-                k = 0;
-            }
-            nq = s.end[k];
-            h += s.tail[k];
-            // heads here (an open chunk's head is all of it); tails of handed-over chunks
-            // were validated by the follow walk
-            const uint64_t off = first_bad(P.in, b0, b0 + c.m, d.A);
-            if (off < b0 + c.m) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
-        }
-        if (P.fchunk_q) {
-            P.fchunk_q[i] = q;
-            P.fchunk_h[i] = h;
-        }
-        uint64_t rc = 1;
-        if (i > 0) {
-            const uint32_t cl = P.in[b0 - 1];
-            const uint32_t li = (P.cand == PAREM_CANDIDATES_ENUM || cl >= d.A) ? d.A : cl;
-            rc = route_count(P, cl, P.in[b0], __ldg(d.Lcnt + li));
-        }
-        routes += rc;
-        steps += rc * (b1 - b0);
-        hits += h;
-        q = nq;
-    }
-    P.hdr->final_q = q;
-    P.hdr->hits = hits;
-    P.hdr->routes = routes;
-    P.hdr->steps = steps;
-}
 
 // E5: every chunk's entering state and hits (thread per block walking its kBlk maps), the
 // total, and the result (last CTA).
@@ -899,6 +922,7 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     conv_follow_kernel<SMEM, W32><<<g2, kFollowThreads, tb, s>>>(P);
     prof_after("conv_follow", s);
     conv_ends_kernel<<<g2, kFollowThreads, 0, s>>>(P);
+    conv_wide_kernel<W32><<<1, 32, 0, s>>>(P);
 
     int bpm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, conv_map_kernel<SMEM, W32>, kSetWarps * 32, tb);
@@ -914,7 +938,6 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     conv_super_kernel<<<(unsigned)((nsb * 32 + kFollowThreads - 1) / kFollowThreads), kFollowThreads, 0, s>>>(P);
     conv_path_kernel<<<1, 32, 0, s>>>(P);
     conv_blockin_kernel<<<(unsigned)((nsb + kFollowThreads - 1) / kFollowThreads), kFollowThreads, 0, s>>>(P);
-    conv_seq_kernel<W32><<<1, 32, 0, s>>>(P);
     prof_after("conv_join", s);
     conv_resolve_kernel<<<(unsigned)((nb + kFollowThreads - 1) / kFollowThreads), kFollowThreads, 0, s>>>(P);
     prof_after("conv_resolve", s);

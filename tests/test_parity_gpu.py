@@ -560,3 +560,27 @@ def test_lookback_rejected_off_tiny(parem, torch_mod):
             d.match(to_dev(torch_mod, c.make_input()), parem.options(candidates="lookback", lookback=4))
         with pytest.raises(parem.ParemError):
             d.match(to_dev(torch_mod, c.make_input()), parem.options(candidates="lookback"))
+
+
+def test_conv_wide_chunks(parem, torch_mod):
+    """Chunks whose candidate set never shrinks to 32 states ("wide"): symbol 0 permutes the
+    64 states (a rotation), symbols 1..3 are random maps, so the DFA converges on random
+    input (converging path chosen) but long runs of symbol 0 keep every route apart.  Wide
+    chunks are resolved from their entering sets; the rest stays parallel."""
+    Q, A = 64, 4
+    rng = np.random.default_rng(64)
+    t = np.empty((Q, A), dtype=np.uint16)
+    t[:, 0] = (np.arange(Q) + 1) % Q
+    t[:, 1:] = rng.integers(0, Q, (Q, 3))
+    acc = rng.random(Q) < 0.2
+    n = 1 << 21
+    x = rng.integers(1, 4, n).astype(np.uint8)
+    for start in rng.integers(0, n - 200_000, 6):
+        x[start:start + int(rng.integers(10_000, 200_000))] = 0
+    with parem.Dfa(t, 3, acc) as d:
+        assert d.plan(n)["kernel"] == 3
+    for L in (0, 4096, 20_000):
+        check(parem, torch_mod, t, 3, acc, x, parem.options(chunk_len=L, kernel="conv"))
+    check_find(parem, torch_mod, t, 3, acc, x, parem.options(kernel="conv", chunk_len=4096), cap=5000)
+    xz = np.zeros(300_001, np.uint8)   # every chunk wide
+    check(parem, torch_mod, t, 3, acc, xz, parem.options(chunk_len=4096, kernel="conv"))
