@@ -161,7 +161,9 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
             if (L % 128 == 0) L += 16;
         }
         if (L > (1ull << 30)) L = 1ull << 30;
-        const uint64_t p = n / L ? n / L : 1;
+        // planner-chosen lengths: the remainder forms a SHORTER last chunk (p = ceil(n / L)),
+        // so no follow thread walks more than L bytes (a forced chunk_len keeps reading C7)
+        const uint64_t p = forced ? (n / L ? n / L : 1) : ceil_div(n, L);
         plan->policy = PAREM_BOUNDARY_GRID;   // the converging path uses the paper's partition
         plan->dmax = dmax;
         plan->threads = 512;
