@@ -38,6 +38,25 @@ static int cached_bps(int kind, uint32_t a, uint32_t b, uint32_t c, uint32_t thr
 }
 
 static uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// Tiny kernel: the remainder r = n mod L is walked by the last chunk's thread after its
+// row (reading C7), ~0.7x the time per byte of the streamed rows; longer rows cost every
+// thread.  Among the row lengths L0, L0 + 64, ... (not multiples of 256 B, see
+// profiles/r01_stride_probe.txt) take the one minimising 3 L + 2 r.
+static uint64_t pick_row_len(uint64_t n, uint64_t L0) {
+    uint64_t best = L0, best_cost = ~0ull;
+    for (uint64_t j = 0; j < 64; ++j) {
+        const uint64_t L = L0 + 64 * j;
+        if (L > n) break;
+        if (L % 256 == 0) continue;
+        const uint64_t cost = 3 * L + 2 * (n % L);
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = L;
+        }
+    }
+    return best;
+}
 static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan* plan) {
@@ -117,6 +136,7 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
             L = ceil_div(n, target);
             L = (L + 63) & ~63ull;       // whole TMA boxes per row
             if (L < 64) L = 64;   // one TMA box per row: small inputs still spread over many CTAs
+            L = pick_row_len(n, L);
         }
         plan->tma = stages;
         if (L > (1ull << 30)) L = 1ull << 30;
