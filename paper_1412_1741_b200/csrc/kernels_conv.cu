@@ -922,23 +922,29 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     conv_follow_kernel<SMEM, W32><<<g2, kFollowThreads, tb, s>>>(P);
     prof_after("conv_follow", s);
     conv_ends_kernel<<<g2, kFollowThreads, 0, s>>>(P);
+    prof_after("conv_ends", s);
     conv_wide_kernel<W32><<<1, 32, 0, s>>>(P);
+    prof_after("conv_wide", s);
 
     int bpm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, conv_map_kernel<SMEM, W32>, kSetWarps * 32, tb);
     if (bpm < 1) bpm = 1;
     const unsigned gm = (unsigned)(g1w < (uint64_t)sms * bpm ? g1w : (uint64_t)sms * bpm);
     conv_map1_kernel<W32><<<g2, kFollowThreads, 0, s>>>(P);
-
+    prof_after("conv_map1", s);
     conv_map_kernel<SMEM, W32><<<gm, kSetWarps * 32, tb, s>>>(P);
+    prof_after("conv_map", s);
 
     const uint64_t nb = (P.p + kBlk - 1) / kBlk;
     conv_block_kernel<<<(unsigned)((nb * 32 + kFollowThreads - 1) / kFollowThreads), kFollowThreads, 0, s>>>(P);
+    prof_after("conv_block", s);
     const uint64_t nsb = (nb + kBlk - 1) / kBlk;
     conv_super_kernel<<<(unsigned)((nsb * 32 + kFollowThreads - 1) / kFollowThreads), kFollowThreads, 0, s>>>(P);
+    prof_after("conv_super", s);
     conv_path_kernel<<<1, 32, 0, s>>>(P);
+    prof_after("conv_path", s);
     conv_blockin_kernel<<<(unsigned)((nsb + kFollowThreads - 1) / kFollowThreads), kFollowThreads, 0, s>>>(P);
-    prof_after("conv_join", s);
+    prof_after("conv_blockin", s);
     conv_resolve_kernel<<<(unsigned)((nb + kFollowThreads - 1) / kFollowThreads), kFollowThreads, 0, s>>>(P);
     prof_after("conv_resolve", s);
     e = cudaGetLastError();

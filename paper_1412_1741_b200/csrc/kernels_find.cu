@@ -314,8 +314,11 @@ int launch_find(const Plan& plan, const MatchParams& P, cudaStream_t s) {
         prof_after("find_group", s);
         const uint64_t nsg = (groups + 31) / 32;
         find_super_kernel<<<nblk(nsg * 32, kFindThreads), kFindThreads, 0, s>>>(P, groups);
+        prof_after("find_super", s);
         find_group_seq_kernel<<<1, 32, 0, s>>>(P, groups);
+        prof_after("find_group_seq", s);
         find_group_in_kernel<<<nblk(nsg * 32, kFindThreads), kFindThreads, 0, s>>>(P, groups);
+        prof_after("find_group_in", s);
         find_chunks_kernel<<<nblk(groups, kFindThreads), kFindThreads, 0, s>>>(P, groups);
         prof_after("find_resolve", s);
     } else if (plan.kernel == kKernelLanes) {
@@ -323,7 +326,9 @@ int launch_find(const Plan& plan, const MatchParams& P, cudaStream_t s) {
         prof_after("find_resolve", s);
     }   // converging path: q_i and h_i were written by conv_heads
     find_scan_sums_kernel<<<(unsigned)nb, kScanBlock / 4, 0, s>>>(P);
+    prof_after("find_scan_sums", s);
     find_scan_blocks_kernel<<<1, 32, 0, s>>>(P, nb);
+    prof_after("find_scan_blocks", s);
     find_scan_apply_kernel<<<(unsigned)nb, kScanBlock / 4, 0, s>>>(P);
     prof_after("find_scan", s);
     if (plan.kernel == kKernelTiny) {

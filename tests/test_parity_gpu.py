@@ -388,7 +388,8 @@ def test_profile_records_kernels(parem, torch_mod):
         parem.profile(False)
         recs = parem.profile_read()
     names = [r[1] for r in recs]
-    assert names == ["conv_set", "conv_follow", "conv_join", "conv_resolve"] * 2
+    assert names == ["conv_set", "conv_follow", "conv_ends", "conv_wide", "conv_map1", "conv_map", "conv_block",
+                     "conv_super", "conv_path", "conv_blockin", "conv_resolve"] * 2
     assert {r[0] for r in recs} == {0, 1} and all(r[2] > 0 for r in recs)
 
 
