@@ -324,7 +324,7 @@ int launch_find(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     } else if (plan.kernel == kKernelLanes) {
         find_lanes_seq_kernel<<<1, 32, 0, s>>>(P);
         prof_after("find_resolve", s);
-    }   // converging path: q_i and h_i were written by conv_heads
+    }   // converging path: q_i and h_i were written by conv_resolve
     find_scan_sums_kernel<<<(unsigned)nb, kScanBlock / 4, 0, s>>>(P);
     prof_after("find_scan_sums", s);
     find_scan_blocks_kernel<<<1, 32, 0, s>>>(P, nb);
