@@ -271,10 +271,17 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
                 if (lane == 0) list[0] = (uint16_t)start_state(P, &dead);
             } else {
                 const uint32_t c = in[b0 - 1];
-                const uint32_t li = (P.cand == PAREM_CANDIDATES_ENUM || c >= d.A) ? d.A : c;
-                D = __ldg(d.Lcnt + li);
-                const uint32_t* L = d.Llist + __ldg(d.Loff + li);
-                for (uint32_t k = lane; k < D; k += 32) list[k] = (uint16_t)__ldg(L + k);
+                if (c >= d.A && P.cand != PAREM_CANDIDATES_ENUM) {
+                    // invalid byte (the result is ESYMBOL, reading C11): any candidate will
+                    // do, and all of Q would not fit the list sized for max |L(c)|
+                    D = 1;
+                    if (lane == 0) list[0] = 0;
+                } else {
+                    const uint32_t li = P.cand == PAREM_CANDIDATES_ENUM ? d.A : c;
+                    D = __ldg(d.Lcnt + li);
+                    const uint32_t* L = d.Llist + __ldg(d.Loff + li);
+                    for (uint32_t k = lane; k < D; k += 32) list[k] = (uint16_t)__ldg(L + k);
+                }
             }
             __syncwarp();
             uint64_t pos = b0;
@@ -876,7 +883,9 @@ __global__ void __launch_bounds__(kFollowThreads) conv_resolve_kernel(const Matc
     if (!flag || threadIdx.x != 0) return;
     __threadfence();
     const volatile WsHeader* h = P.hdr;
-    if (h->err & 1u) {   // internal invariant violated: report instead of a wrong answer
+    // internal invariant violated: report instead of a wrong answer -- unless a byte was
+    // outside the alphabet (ESYMBOL wins; such a boundary gets a placeholder candidate)
+    if ((h->err & 1u) && h->bad_inv == 0ull) {
         parem_result r;
         memset(&r, 0, sizeof(r));
         r.final_state = PAREM_DEAD;

@@ -167,9 +167,7 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         if (const char* e = getenv("PAREM_CONV_CHAINS")) chains = strtoull(e, nullptr, 10);   // experiments
         if (const char* e = getenv("PAREM_CONV_DMAX")) dmax = (uint32_t)atoi(e);
         if ((dmax != 1 && dmax != 2) || dfa->conv_t1 == 0) dmax = 4;
-        // forced lengths below 16 B are rounded up on this path (one-byte chunks of a large DFA
-        // trip an unresolved fault in round 1)
-        if (forced) L = forced < 16 ? 16 : forced;
+        if (forced) L = forced;
         else {
             L = ceil_div(n, chains ? chains : 1);
             // chunks >= 16x the probe's convergence length, so open chunks (no hand-over,

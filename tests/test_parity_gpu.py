@@ -585,3 +585,17 @@ def test_conv_wide_chunks(parem, torch_mod):
     check_find(parem, torch_mod, t, 3, acc, x, parem.options(kernel="conv", chunk_len=4096), cap=5000)
     xz = np.zeros(300_001, np.uint8)   # every chunk wide
     check(parem, torch_mod, t, 3, acc, xz, parem.options(chunk_len=4096, kernel="conv"))
+
+
+def test_conv_invalid_byte_before_boundaries(parem, torch_mod):
+    """Regression: an invalid byte right before a chunk boundary on the converging path (its
+    candidate list would be all of Q, larger than the set walk's list) must give ESYMBOL
+    with the smallest offset, for every chunk length down to one byte."""
+    c = synth.config(3, n=50_000)
+    rng = np.random.default_rng(31)
+    for L in (1, 2, 3, 16, 1000):
+        x = c.make_input().copy()
+        bad = np.sort(rng.integers(1, x.size, 3))
+        x[bad] = 250
+        got = check(parem, torch_mod, c.table, c.start, c.accept, x, parem.options(chunk_len=L, kernel="conv"))
+        assert got.status == parem.PAREM_ESYMBOL and got.bad_offset == bad[0]
