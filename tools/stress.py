@@ -6,7 +6,7 @@ import oracle, synth, paper_1412_1741_b200 as P
 
 bad = 0
 for seed in range(int(sys.argv[1]) if len(sys.argv) > 1 else 300):
-    rng = np.random.default_rng(100000 + seed)
+    rng = np.random.default_rng(int(os.environ.get("STRESS_BASE", "100000")) + seed)
     Q = int(rng.choice([1, 2, 4, 9, 17, 32, 33, 64, 200, 700, 3000]))
     A = int(rng.choice([1, 2, 3, 4, 6, 26, 255, 256]))
     partial = rng.random() < 0.3
