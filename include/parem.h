@@ -100,7 +100,8 @@ typedef struct parem_dfa parem_dfa;
 
 /* Create a DFA handle (P:58 quintuple; the table is the paper's adjacency matrix Tt,
  * P:76).
- *   num_states     Q >= 1 (Q <= 65535 for 2-byte tables).
+ *   num_states     1 <= Q <= 4194304 (Q <= 65535 for 2-byte tables); larger -> PAREM_EINVAL
+ *                  (device table offsets are 32-bit).
  *   alphabet_size  A in [1, 256]; symbols are raw byte values 0..A-1 (mapping characters
  *                  to symbols is the caller's job).
  *   table          host pointer, row-major Q x A, table[s*A + c] = delta(s, c), elements of
@@ -257,7 +258,10 @@ int parem_profile_read(parem_kernel_time* out, int max, int* count);
  *   read_stream: 16-B vector loads over n bytes, grid-stride, reduced to *d_sink.
  *   gather:      every thread performs `steps` dependent random lookups into a table of
  *                table_bytes (uint16 entries) held in shared memory (where=0) or global /
- *                L2 (where=1); lookups_out = total lookups per launch. */
+ *                L2 (where=1; indices scattered over the whole table) or in shared memory,
+ *                lane-private (where=2); lookups_out = total lookups per launch.  d_sink[0..1]:
+ *                the kernels write d_sink[0] only if their result equals d_sink[1] (pass
+ *                0xFFFFFFFF there), which keeps the loads alive. */
 float parem_bench_read_stream(const uint8_t* d_input, uint64_t n, uint32_t* d_sink, int reps, void* stream);
 float parem_bench_gather(uint32_t where, const uint16_t* d_table, uint32_t table_entries, uint32_t steps,
                          uint32_t* d_sink, uint64_t* lookups_out, int reps, void* stream);

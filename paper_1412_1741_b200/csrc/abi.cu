@@ -4,7 +4,10 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "kernels_common.cuh"
@@ -74,6 +77,19 @@ void prof_begin(cudaStream_t s) {
 }
 }  // namespace
 
+cudaError_t smem_optin(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> cur;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    size_t& have = cur[{fn, dev}];
+    if (bytes <= have) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
+
 void prof_after(const char* name, cudaStream_t s) {
     ProfState& p = g_prof;
     if (!p.active) return;
@@ -118,6 +134,8 @@ static int match_impl(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, 
     P.slots = plan.slots;
     P.tg = plan.tg;
     P.dmax = plan.dmax;
+    P.conv_cpt = plan.conv_cpt;
+    P.set_own = plan.set_own;
     P.lookback = opts ? opts->lookback : 0;
     P.offset_base = offset_base;
     P.carry = d_carry;
@@ -330,13 +348,14 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint16_t* __restrict_
             if (WHERE == 0) v = t32[x[k]];
             else if (WHERE == 1) v = __ldg(tab + x[k]);
             else v = t32[x[k] * 32u + lane];
-            x[k] = (v + s) & mask;
+            // scatter over the WHOLE table (v alone would only reach the first 64 Ki entries)
+            x[k] = (v * 0x9E3779B1u + s) & mask;
         }
     }
     uint32_t acc = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc ^= x[k];
-    if (acc == 0xFFFFFFFFu) sink[0] = acc;
+    if (acc == sink[1]) sink[0] = acc;   // the caller's sink[1] is never a reachable value
 }
 
 }  // namespace parem
@@ -423,7 +442,7 @@ extern "C" float parem_bench_gather(uint32_t where, const uint16_t* d_table, uin
     if (smem > 200 * 1024) return (float)PAREM_EINVAL;
     const void* fn = where == 0 ? (const void*)gather_kernel<0> : where == 1 ? (const void*)gather_kernel<1>
                                                                            : (const void*)gather_kernel<2>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_optin(fn, smem);
     int bps = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, 256, smem);
     if (bps < 1) bps = 1;

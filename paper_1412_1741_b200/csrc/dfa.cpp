@@ -53,7 +53,9 @@ extern "C" int parem_dfa_create(uint32_t Q, uint32_t A, const void* table, uint3
     if (A == 0 || A > 256) { set_error("alphabet_size must be in [1, 256]"); return PAREM_EINVAL; }
     if (eb != 2 && eb != 4) { set_error("elem_bytes must be 2 or 4"); return PAREM_EINVAL; }
     if (eb == 2 && Q > 65535) { set_error("uint16 tables need num_states <= 65535"); return PAREM_EINVAL; }
-    if (Q > (1u << 30)) { set_error("num_states too large"); return PAREM_EINVAL; }
+    // device table offsets are u32 (symbol-major lanes table: Apad * Qpad * 4 bytes < 2^32)
+    // and the accept bit sits above dest * 4 in a u32 entry: Q <= 2^22 keeps both exact
+    if (Q > (1u << 22)) { set_error("num_states %u > 4194304 is not supported", Q); return PAREM_EINVAL; }
     if (start >= Q) { set_error("start_state %u >= num_states %u", start, Q); return PAREM_EINVAL; }
     const uint32_t dead_in = eb == 2 ? 0xFFFFu : 0xFFFFFFFFu;
 
@@ -210,7 +212,11 @@ extern "C" int parem_dfa_create(uint32_t Q, uint32_t A, const void* table, uint3
         std::vector<uint32_t> mark(Qp, 0);
         for (uint32_t s = 0; s < Qp; ++s) cur[s] = s;
         uint64_t x = 0x9E3779B97F4A7C15ull;
-        for (uint32_t t = 1; t <= (1u << 16) && cur.size() > 1; ++t) {
+        // bounded by total work (<= 2^27 lookups): a DFA whose routes never merge (e.g.
+        // permutation columns) ends the probe early and stays off the converging path
+        uint64_t work = 0;
+        for (uint32_t t = 1; t <= (1u << 16) && cur.size() > 1 && work < (1ull << 27); ++t) {
+            work += cur.size();
             x += 0x9E3779B97F4A7C15ull;
             uint64_t z = x;
             z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;

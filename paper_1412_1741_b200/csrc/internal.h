@@ -13,6 +13,7 @@
 //     the next byte offset is (entry & SMASK) | (c << SHC) -- one LOP3 per lookup.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stddef.h>
@@ -68,6 +69,8 @@ struct MatchParams {
     uint32_t stages;           // tiny: TMA stages per warp (0 = no TMA)
     uint32_t dmax;             // conv: survivors handed from the set walk to the follow walk
     uint32_t lookback;         // tiny: k of the look-back candidate rule
+    uint32_t conv_cpt;         // conv: chunks per follow thread
+    uint32_t set_own;          // conv: phase-A dedup by owner tags (else image bitmap + atomics)
     uint64_t offset_base;
     const parem_result* carry; // may be null
     parem_result* result;
@@ -102,6 +105,11 @@ struct Plan {
     uint32_t smem_tab;       // lanes: table staged in shared memory
     uint32_t tma;            // tiny: TMA stages per warp (0 = rows read with 16-B loads)
     uint32_t dmax;           // conv: set-walk hand-over threshold (1, 2 or 4 survivors)
+    uint32_t conv_tma;       // conv: TMA-staged follow walk (rows of L bytes)
+    uint32_t set_own;        // conv: phase-A dedup by owner tags (Qpad <= 1024)
+    uint32_t conv_cpt;       // conv: chunks per follow thread (1 or 2)
+    uint32_t conv_fthreads;  // conv: follow block size
+    uint32_t conv_swarps;    // conv: set-walk warps per CTA
     size_t smem;
     size_t ws;
     size_t off_maps, off_hits;
@@ -129,6 +137,12 @@ namespace parem {
 void set_error(const char* fmt, ...);
 // per-kernel timing (parem_profile): call after each kernel launch of a match
 void prof_after(const char* name, cudaStream_t s);
+// Raise a kernel's dynamic shared memory limit to at least `bytes`, under a mutex, never
+// lowering it: the attribute is process-wide, so a concurrent match on another host thread
+// can never see it drop below what its own launch needs.  Keeping it at the
+// largest size actually launched (rather than the opt-in maximum) leaves the driver's
+// shared/L1 carveout choice to the real footprint.
+cudaError_t smem_optin(const void* fn, size_t bytes);
 int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan* plan);
 // device side (kernels_*.cu)
 int launch_tiny(const Plan& plan, const MatchParams& P, cudaStream_t s);
@@ -138,8 +152,10 @@ int launch_find(const Plan& plan, const MatchParams& P, cudaStream_t s);
 size_t find_extra_bytes(const Plan& plan, const DevDfa& d);
 void find_bind(const Plan& plan, MatchParams& P, unsigned char* extra);
 size_t conv_ws_total(uint64_t p);
-size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap);
+size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap, uint32_t warps);
 int launch_trivial(const MatchParams& P, cudaStream_t s);
+bool encode_rows_map(CUtensorMap* map, const uint8_t* base, uint64_t row_len, uint64_t rows, uint32_t box_w,
+                     uint32_t box_rows);
 int tiny_blocks_per_sm(uint32_t K, uint32_t B, bool tma, size_t smem);
 size_t tiny_smem_bytes(const DevDfa& d, uint32_t B, uint32_t stages);
 uint32_t tiny_pick_stages(const DevDfa& d, uint32_t B);

@@ -24,6 +24,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string.h>
+
+#include <mutex>
 #include <type_traits>
 
 #include "kernels_common.cuh"
@@ -114,12 +117,13 @@ __device__ __forceinline__ ConvWs conv_ws(const MatchParams& P) {
 
 __host__ __device__ __forceinline__ size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
 
-// K1 per-warp scratch: the candidate list (u16 state indices, compacted in place) and a
-// |Q|-bit image bitmap.
+// K1 per-warp scratch: the candidate list (u16 state indices, compacted in place) and, for
+// Qpad <= 256, the owner tags (u16 per state: the list index that last produced the
+// state), else a Qpad-bit image bitmap (atomicOr; the tags would cost the occupancy).
 constexpr int kPark = 4;   // parked chunks per warp in the set walk's phase B
+constexpr uint32_t kOwnerMaxQ = 256;   // measured: tags win on cfg3 (256 states), lose on cfg5 (1024)
 __host__ __device__ __forceinline__ size_t set_warp_bytes(uint32_t cap, uint32_t Qpad) {
-    // list | image bitmap | parked slots: start state per lane, D and phase-B start offset
-    return al16(2 * (size_t)cap) + al16((size_t)(Qpad + 31) / 32 * 4);
+    return al16(2 * (size_t)cap) + (Qpad <= kOwnerMaxQ ? al16(2 * (size_t)Qpad) : al16((size_t)(Qpad + 31) / 32 * 4));
 }
 
 __host__ __device__ __forceinline__ size_t tab_bytes(const DevDfa& d) {
@@ -131,6 +135,7 @@ __host__ __device__ __forceinline__ size_t tab_bytes(const DevDfa& d) {
 template <bool SMEM, bool W32>
 struct Tab {
     static constexpr uint32_t ES = W32 ? 4 : 2, ACC = W32 ? 31 : 15;
+    static constexpr bool kSmem = SMEM, kW32 = W32;
     const unsigned char* g;
     uint32_t cbase, COL, SMASK, CMASK;
 
@@ -142,6 +147,8 @@ struct Tab {
         cbase = SMEM ? sbase : 0u;
     }
     __device__ __forceinline__ uint32_t col(uint32_t c) const { return (c & CMASK) * COL + cbase; }
+    // column of an input byte already masked to (c & CMASK) by a whole-word AND
+    __device__ __forceinline__ uint32_t colm(uint32_t c) const { return c * COL + cbase; }
     __device__ __forceinline__ uint32_t at(uint32_t off) const {
         uint32_t v;
         if constexpr (SMEM) {
@@ -156,6 +163,8 @@ struct Tab {
     __device__ __forceinline__ uint32_t next(uint32_t e, uint32_t colc) const { return at((e & SMASK) | colc); }
     __device__ __forceinline__ uint32_t state(uint32_t e) const { return (e & SMASK) / ES; }
     __device__ __forceinline__ uint32_t hit(uint32_t e) const { return e >> ACC; }
+    __device__ __forceinline__ uint32_t start(uint32_t s) const { return s * ES; }
+    __device__ __forceinline__ uint32_t word_mask() const { return CMASK * 0x01010101u; }
 };
 
 // Stage the symbol-major table into shared memory at an address that is a multiple of its
@@ -184,12 +193,15 @@ __device__ __forceinline__ uint64_t conv_b(const MatchParams& P, uint64_t i) {
 
 // ---------------------------------------------------------------------------------------
 // K1: set walk.  Persistent warps take chunks in turn; R_t is deduplicated every step
-// through an image bitmap (phase A) until <= 32 states remain.  The chunk is then PARKED in
-// one of kPark register slots (one state per lane, duplicates allowed) and the warp
-// advances all its parked chunks together, 32 bytes at a time -- kPark independent lookup
-// chains per lane -- counting distinct states with __match_any_sync, until <= dmax remain
-// (hand-over) or the chunk ends (open).  A freed slot is refilled by the next chunk's phase A.
-template <bool SMEM, bool W32>
+// (phase A) until <= 32 states remain.  For Qpad <= 256 each element writes its list
+// index into the owner tag of the state it reaches (plain shared stores, last writer
+// wins), and after a warp barrier exactly one element per distinct state reads its own
+// index back -- no atomics, no bitmap to clear; larger Q uses an image bitmap and atomicOr.
+// The chunk is then PARKED in one of kPark register slots (one state per lane) and the
+// warp advances its parked chunks together, 32 bytes at a time (kPark independent lookup
+// chains per lane), counting distinct states with __match_any_sync after every 32 bytes.
+// A chunk leaves phase B when <= dmax states remain (hand-over) or at its end (open).
+template <bool SMEM, bool W32, bool OWN>
 __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchParams P) {
     extern __shared__ __align__(16) unsigned char sm[];
     const DevDfa& d = P.d;
@@ -200,8 +212,9 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
     T.init(d, stage_table<SMEM, W32>(d, sm));
     __syncthreads();
     unsigned char* ws = sm + tb + warp * set_warp_bytes(cap, d.Qpad);
-    uint16_t* list = reinterpret_cast<uint16_t*>(ws);   // compacted in place
-    uint32_t* bm = reinterpret_cast<uint32_t*>(ws + al16(2 * (size_t)cap));
+    uint16_t* list = reinterpret_cast<uint16_t*>(ws);   // state indices, compacted in place
+    uint16_t* owner = reinterpret_cast<uint16_t*>(ws + al16(2 * (size_t)cap));
+    uint32_t* bm = reinterpret_cast<uint32_t*>(owner);
     const uint32_t nbm = (d.Qpad + 31) / 32;
     const uint8_t* in = P.in;
     const uint32_t ltmask = (1u << lane) - 1u;
@@ -209,12 +222,13 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
     const ConvWs W = conv_ws(P);
     ConvChunk* infos = W.info;
 
+    // distinct states among the warp's lanes (lanes past |R| duplicate lane 0)
     auto distinct = [&](uint32_t e, uint32_t& leaders) {
-        const uint32_t m = __match_any_sync(0xFFFFFFFFu, T.state(e));
+        const uint32_t m = __match_any_sync(0xFFFFFFFFu, e & T.SMASK);
         leaders = __ballot_sync(0xFFFFFFFFu, (__ffs(m) - 1) == (int)lane);
         return (uint32_t)__popc(leaders);
     };
-    // a chunk whose set never shrank to 32 states: no survivors (sequential fallback)
+    // a chunk whose set never shrank to 32 states: no survivors (resolved in order later)
     auto write_wide = [&](uint64_t t, uint64_t b0, uint64_t b1) {
         if (lane == 0) {
             infos[t].m = (uint32_t)(b1 - b0);
@@ -285,39 +299,70 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
             }
             __syncwarp();
             uint64_t pos = b0;
-            // phase A: more than 32 states -- the deduplicated image every step, compacted
-            // in place (a batch is read into registers before any of its writes land, and
-            // writes never pass the batch being read)
+            // phase A: more than 32 states -- the deduplicated image every step
             while (D > 32 && pos < b1) {
                 const uint32_t colc = T.col(__ldg(in + pos));
-                for (uint32_t i = lane; i < nbm; i += 32) bm[i] = 0u;
-                __syncwarp();
                 uint32_t nD = 0;
-                for (uint32_t base = 0; base < D; base += 128) {
-                    uint32_t ns[4];
-                    bool fresh[4];
+                if constexpr (OWN) {
+                    // pass 1: image of every element, in place; owner tag of its state
+                    for (uint32_t base = 0; base < D; base += 128) {
+                        uint32_t ns[4];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const uint32_t idx = base + 32u * j + lane;
-                        ns[j] = idx < D ? T.state(T.next(list[idx] * T.ES, colc)) : 0xFFFFFFFFu;
-                    }
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t i = base + 32u * j + lane;
+                            ns[j] = i < D ? T.state(T.next(list[i] * T.ES, colc)) : 0u;
+                        }
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        fresh[j] = false;
-                        if (ns[j] != 0xFFFFFFFFu) {
-                            const uint32_t bit = 1u << (ns[j] & 31u);
-                            fresh[j] = !(atomicOr(bm + (ns[j] >> 5), bit) & bit);
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t i = base + 32u * j + lane;
+                            if (i < D) {
+                                list[i] = (uint16_t)ns[j];
+                                owner[ns[j]] = (uint16_t)i;
+                            }
                         }
                     }
                     __syncwarp();
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, fresh[j]);
-                        if (fresh[j]) list[nD + __popc(bal & ltmask)] = (uint16_t)ns[j];
+                    // pass 2: the element that owns its state survives; compaction in place
+                    for (uint32_t base = 0; base < D; base += 32) {
+                        const uint32_t i = base + lane;
+                        const uint32_t v = i < D ? list[i] : 0u;
+                        const bool fresh = i < D && owner[v] == (uint16_t)i;
+                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, fresh);
+                        if (fresh) list[nD + __popc(bal & ltmask)] = (uint16_t)v;
                         nD += __popc(bal);
                     }
+                } else {
+                    // large Q: image bitmap, atomicOr decides the first arrival (a batch is
+                    // read into registers before any of its writes land)
+                    for (uint32_t i = lane; i < nbm; i += 32) bm[i] = 0u;
                     __syncwarp();
+                    for (uint32_t base = 0; base < D; base += 128) {
+                        uint32_t ns[4];
+                        bool fresh[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t idx = base + 32u * j + lane;
+                            ns[j] = idx < D ? T.state(T.next(list[idx] * T.ES, colc)) : 0xFFFFFFFFu;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            fresh[j] = false;
+                            if (ns[j] != 0xFFFFFFFFu) {
+                                const uint32_t bit = 1u << (ns[j] & 31u);
+                                fresh[j] = !(atomicOr(bm + (ns[j] >> 5), bit) & bit);
+                            }
+                        }
+                        __syncwarp();
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, fresh[j]);
+                            if (fresh[j]) list[nD + __popc(bal & ltmask)] = (uint16_t)ns[j];
+                            nD += __popc(bal);
+                        }
+                        __syncwarp();
+                    }
                 }
+                if constexpr (OWN) __syncwarp();
                 D = nD;
                 ++pos;
             }
@@ -349,7 +394,9 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
             occ |= 1u << k;
         }
         if (!occ) break;
-        // ---- phase B: advance every parked chunk by up to 32 bytes, chains interleaved ----
+        // ---- phase B: advance every parked chunk by up to 32 bytes, chains interleaved
+        // (lanes whose routes met keep walking in lock-step: the same address costs no
+        // extra L1TEX wavefront) ----
         uint32_t cnt[kPark], mine[kPark], cmax = 0;
 #pragma unroll
         for (int j = 0; j < kPark; ++j) {
@@ -382,128 +429,366 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
 }
 
 // ---------------------------------------------------------------------------------------
-// K2: follow the survivors over the rest of the chunk, thread per chunk, K routes in
-// registers with K = the warp's largest survivor count (1, 2 or 4); once every lane of the
-// warp has all its routes in one state (warp-uniform), one route is advanced and the
-// others rebuilt exactly (end shared, hits + the offset at the merge point).
-template <int K, bool SMEM, bool W32>
-__device__ __forceinline__ uint32_t follow_vecs(const Tab<SMEM, W32>& T, const uint8_t* p, uint32_t v, uint32_t nv,
-                                                uint32_t nvmax, uint32_t A, uint32_t* e, uint32_t* h, uint32_t& bad) {
-    // the next 16 bytes are loaded while the current ones are walked (one vector in flight
-    // per thread hides the HBM latency behind the dependent lookups)
-    uint4 nx = v < nv ? ldg_v4_na(p + 16ull * v) : make_uint4(0, 0, 0, 0);
-    for (; v < nvmax; ++v) {
-        const uint4 x = nx;
-        if (v + 1 < nv) nx = ldg_v4_na(p + 16ull * (v + 1));
-        if (v < nv) {
-            bad |= badbits(x.x, A) | badbits(x.y, A) | badbits(x.z, A) | badbits(x.w, A);
-            const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+// K2: follow the survivors over the rest of the chunk, thread per chunk (CPT chunks per
+// thread, interleaved: CPT independent chains), K routes per chunk in registers with K =
+// the warp's largest survivor count (4, or 1); routes k >= D of a chunk are predicated
+// off.  Once every lane of the warp has all its routes in one state (warp-uniform), one
+// route is advanced and the others rebuilt exactly (end shared, hits + the offset at the
+// merge point).
+template <class TT, int CPT>
+struct Follow {
+    const TT& T;
+    const uint8_t* p[CPT];
+    uint32_t nv[CPT], D[CPT];
+    uint32_t e[CPT][kDMax], h[CPT][kDMax];
+    uint32_t bad, A, wmask, K, K7F;   // K = (256 - A) per byte, K7F = K & 0x7F7F7F7F
+    bool check;
+
+    __device__ __forceinline__ Follow(const TT& t) : T(t) {}
+
+    template <int K>
+    __device__ __forceinline__ void word(int j, uint32_t w) {
+        if (check) {
+            // bytes >= A (reading C11): b >= A iff b + (256 - A) carries out of bit 7 = the
+            // majority of (b7, K7, carry into bit 7); accumulated, tested once at the end
+            const uint32_t t = (w & 0x7F7F7F7Fu) + K7F;
+            bad |= (w & K) | ((w | K) & t);
+        }
+        const uint32_t wm = w & wmask;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+        for (uint32_t b = 0; b < 4; ++b) {
+            const uint32_t colc = T.colm(__byte_perm(wm, 0u, 0x4440u | b));
 #pragma unroll
-                for (uint32_t b = 0; b < 4; ++b) {
-                    const uint32_t colc = T.col(__byte_perm(w4[q], 0u, 0x4440u | b));
+            for (int k = 0; k < K; ++k) {
+                if (K == 1 || (uint32_t)k < D[j]) {
+                    e[j][k] = T.next(e[j][k], colc);
+                    h[j][k] += T.hit(e[j][k]);
+                }
+            }
+        }
+    }
+
+    // Walk the 16-byte vectors of every chunk (warp-uniform bound nvmax) with PF vectors
+    // per chain in flight (a register ring: a thread-per-chunk stream needs ~64 B in flight
+    // per chain to cover HBM latency behind the dependent lookups; one vector was not
+    // enough, tools/gather_probe.cu rep16).  Routes run K = kDMax wide until every lane of
+    // the warp has all routes of all its chunks in one state (warp-uniform, checked every 4
+    // vectors), then one route per chunk; the others are rebuilt at the end (rebuild()).
+    static constexpr int PF = CPT == 1 ? 4 : 2;
+    bool merged;
+    uint32_t e0[CPT], h0[CPT];
+
+    __device__ __forceinline__ void run(uint32_t nvmax, bool multi) {
+        merged = !multi;
+        uint4 ring[CPT][PF];
 #pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        e[k] = T.next(e[k], colc);
-                        h[k] += T.hit(e[k]);
+        for (int j = 0; j < CPT; ++j)
+#pragma unroll
+            for (int u = 0; u < PF; ++u)
+                ring[j][u] = (uint32_t)u < nv[j] ? ldg_v4_na(p[j] + 16ull * u) : make_uint4(0, 0, 0, 0);
+        for (uint32_t v = 0; v < nvmax; v += PF) {
+#pragma unroll
+            for (int u = 0; u < PF; ++u) {
+                const uint32_t vv = v + u;
+                uint4 x[CPT];
+#pragma unroll
+                for (int j = 0; j < CPT; ++j) {
+                    x[j] = ring[j][u];
+                    if (vv + PF < nv[j]) ring[j][u] = ldg_v4_na(p[j] + 16ull * (vv + PF));
+                }
+                if (merged) {
+#pragma unroll
+                    for (int j = 0; j < CPT; ++j)
+                        if (vv < nv[j]) {
+                            word<1>(j, x[j].x);
+                            word<1>(j, x[j].y);
+                            word<1>(j, x[j].z);
+                            word<1>(j, x[j].w);
+                        }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < CPT; ++j)
+                        if (vv < nv[j]) {
+                            word<kDMax>(j, x[j].x);
+                            word<kDMax>(j, x[j].y);
+                            word<kDMax>(j, x[j].z);
+                            word<kDMax>(j, x[j].w);
+                        }
+                    if ((vv & 3u) == 3u) {
+                        bool conv = true;
+#pragma unroll
+                        for (int j = 0; j < CPT; ++j)
+#pragma unroll
+                            for (int k = 1; k < (int)kDMax; ++k)
+                                conv &= (uint32_t)k >= D[j] || T.state(e[j][k]) == T.state(e[j][0]);
+                        if (__all_sync(0xFFFFFFFFu, conv)) {
+                            merged = true;
+#pragma unroll
+                            for (int j = 0; j < CPT; ++j) {
+                                e0[j] = e[j][0];
+                                h0[j] = h[j][0];
+                            }
+                        }
                     }
                 }
+            }
         }
-        if (K > 1 && (v & 3u) == 3u) {
-            bool conv = true;
+        if (multi && merged) {   // rebuild the routes that were carried by route 0
 #pragma unroll
-            for (int k = 1; k < K; ++k) conv &= T.state(e[k]) == T.state(e[0]);
-            if (__all_sync(0xFFFFFFFFu, conv)) return v + 1;
+            for (int j = 0; j < CPT; ++j)
+#pragma unroll
+                for (int k = 1; k < (int)kDMax; ++k)
+                    if ((uint32_t)k < D[j]) {
+                        h[j][k] = h[j][0] + (h[j][k] - h0[j]);   // u32 wrap-around is exact here
+                        e[j][k] = e[j][0];
+                    }
         }
     }
-    return v;
-}
 
-template <bool SMEM, bool W32>
-__global__ void __launch_bounds__(kFollowThreads) conv_follow_kernel(const MatchParams P) {
-    extern __shared__ __align__(16) unsigned char sm[];
-    const DevDfa& d = P.d;
-    Tab<SMEM, W32> T;
-    T.init(d, stage_table<SMEM, W32>(d, sm));
-    __syncthreads();
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool live = t < P.p;
-    const ConvWs W = conv_ws(P);
-    ConvChunk* info = W.info + (live ? t : 0);
-    const uint64_t b0 = conv_b(P, t), b1 = live ? conv_b(P, t + 1) : b0;
-    const uint32_t D0 = live ? info->D : 0u;
-    const uint32_t D = D0 == kWide ? 0u : D0;   // follow only handed-over chunks
-    const bool act = D != 0;
-    uint64_t a = act ? b0 + info->m : b1;
-    uint32_t e[kDMax], h[kDMax];
-#pragma unroll
-    for (int k = 0; k < (int)kDMax; ++k) {
-        e[k] = act ? info->z[k] * T.ES : 0u;
-        h[k] = 0;
-    }
-    const uint8_t* in = P.in;
-    const uint32_t A = d.A;
-    uint32_t bad = 0;
-    auto stepK = [&](uint32_t c) {
+    __device__ __forceinline__ void step1(int j, uint32_t c) {
+        if (check && c >= A) bad |= 0x80u;
         const uint32_t colc = T.col(c);
 #pragma unroll
+        for (int k = 0; k < (int)kDMax; ++k)
+            if ((uint32_t)k < D[j]) {
+                e[j][k] = T.next(e[j][k], colc);
+                h[j][k] += T.hit(e[j][k]);
+            }
+    }
+};
+
+template <class TT, int CPT>
+__global__ void __launch_bounds__(1024) conv_follow_kernel(const MatchParams P) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const DevDfa& d = P.d;
+    TT T;
+    T.init(d, stage_table<TT::kSmem, TT::kW32>(d, sm));
+    __syncthreads();
+    const ConvWs W = conv_ws(P);
+    const uint8_t* in = P.in;
+    Follow<TT, CPT> F(T);
+    F.bad = 0;
+    F.A = d.A;
+    F.check = d.A < 256;
+    F.K = ((256u - d.A) & 0xFFu) * 0x01010101u;
+    F.K7F = F.K & 0x7F7F7F7Fu;
+    F.wmask = T.word_mask();
+    uint64_t t[CPT], a[CPT], b1[CPT];
+    bool act[CPT];
+    const uint64_t tb = (uint64_t)blockIdx.x * blockDim.x * CPT + threadIdx.x;
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+        t[j] = tb + (uint64_t)j * blockDim.x;
+        const bool live = t[j] < P.p;
+        const ConvChunk* info = W.info + (live ? t[j] : 0);
+        const uint64_t b0 = conv_b(P, t[j]);
+        b1[j] = live ? conv_b(P, t[j] + 1) : b0;
+        const uint32_t D0 = live ? info->D : 0u;
+        F.D[j] = D0 == kWide ? 0u : D0;   // follow only handed-over chunks
+        act[j] = F.D[j] != 0;
+        a[j] = act[j] ? b0 + info->m : b1[j];
+#pragma unroll
         for (int k = 0; k < (int)kDMax; ++k) {
-            e[k] = T.next(e[k], colc);
-            h[k] += T.hit(e[k]);
+            F.e[j][k] = act[j] ? T.start(info->z[k]) : 0u;
+            F.h[j][k] = 0;
         }
-    };
-    // unaligned head (< 16 bytes)
-    const uint64_t mis = act ? (uint64_t)(((uintptr_t)(in + a)) & 15u) : 0u;
-    uint64_t hd = mis ? a + (16 - mis) : a;
-    if (hd > b1) hd = b1;
-    for (; a < hd; ++a) {
-        const uint32_t c = in[a];
-        bad |= c >= A;
-        stepK(c);
+        // unaligned head (< 16 bytes)
+        const uint64_t mis = act[j] ? (uint64_t)(((uintptr_t)(in + a[j])) & 15u) : 0u;
+        uint64_t hd = mis ? a[j] + (16 - mis) : a[j];
+        if (hd > b1[j]) hd = b1[j];
+        for (; a[j] < hd; ++a[j]) F.step1(j, in[a[j]]);
+        F.nv[j] = act[j] ? (uint32_t)((b1[j] - a[j]) >> 4) : 0u;
+        F.p[j] = in + a[j];
     }
     // 16-byte vectors: a warp-uniform trip count (lanes past their own end idle) and a
     // warp-uniform route count
-    const uint32_t nv = act ? (uint32_t)((b1 - a) >> 4) : 0u;
-    uint32_t nvmax = nv, Dw = D;
+    uint32_t nvmax = 0, Dw = 0;
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+        nvmax = max(nvmax, F.nv[j]);
+        Dw = max(Dw, F.D[j]);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         nvmax = max(nvmax, __shfl_xor_sync(0xFFFFFFFFu, nvmax, o));
         Dw = max(Dw, __shfl_xor_sync(0xFFFFFFFFu, Dw, o));
     }
-    const uint8_t* p = in + a;
-    uint32_t v = 0;
-    if (Dw > 2) v = follow_vecs<4>(T, p, v, nv, nvmax, A, e, h, bad);
-    else if (Dw == 2) v = follow_vecs<2>(T, p, v, nv, nvmax, A, e, h, bad);
-    if (v < nvmax) {   // one route per chunk for the rest; rebuild the others exactly
-        const uint32_t e0 = e[0], h0 = h[0];
-        v = follow_vecs<1>(T, p, v, nv, nvmax, A, e, h, bad);
+    F.run(nvmax, Dw > 1);
 #pragma unroll
-        for (int k = 1; k < (int)kDMax; ++k) {
-            if (Dw > 1 || T.state(e[k]) == T.state(e0)) {
-                h[k] = h[0] + (h[k] - h0);   // u32 wrap-around is exact here
-                e[k] = e[0];
+    for (int j = 0; j < CPT; ++j) {
+        a[j] += (uint64_t)F.nv[j] << 4;
+        for (; act[j] && a[j] < b1[j]; ++a[j]) F.step1(j, in[a[j]]);
+    }
+    const bool anybad = (F.bad & 0x80808080u) != 0;
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+        if (!act[j]) continue;
+        SurvRec& sr = W.surv[t[j]];
+        const ConvChunk* info = W.info + t[j];
+        sr.n = F.D[j];
+#pragma unroll
+        for (int k = 0; k < (int)kDMax; ++k)
+            if ((uint32_t)k < F.D[j]) {
+                sr.z[k] = info->z[k];
+                sr.end[k] = T.state(F.e[j][k]);
+                sr.tail[k] = F.h[j][k];
             }
+        if (anybad) {
+            const uint64_t off = first_bad(in, conv_b(P, t[j]) + info->m, b1[j], d.A);
+            if (off < b1[j]) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
         }
     }
-    a += (uint64_t)nv << 4;
-    for (; act && a < b1; ++a) {
-        const uint32_t c = in[a];
-        bad |= c >= A;
-        stepK(c);
+}
+
+// K2 with TMA-staged input (the default): chunk t is row t of a 2-D tensor view of the
+// input (row length L); each warp owns 32 consecutive chunks and streams them through
+// shared memory in 32-row x 64-byte boxes (cp.async.bulk.tensor.2d, SWIZZLE_64B, two
+// mbarrier stages), so the input costs one TMA transaction per 2 KB instead of 32 L1TEX
+// wavefronts per 16-byte vector load of a thread-per-chunk stream (the follow walk was
+// L1TEX-bound: profiles/r02_ncu_*follow*).  A lane walks its head remainder (from b_t + m_t
+// to the next 16-byte unit) from global memory, then its staged units; the last chunk
+// (not a full row) is walked from global memory.
+constexpr uint32_t kFBox = 64, kFStages = 2, kFStageBytes = 32 * kFBox, kFThreads = 512;
+
+__host__ __device__ __forceinline__ size_t follow_tma_smem(size_t tb) {
+    return ((tb + 1023) & ~(size_t)1023) + (kFThreads / 32) * (kFStages * kFStageBytes + 8 * kFStages) + 1024;
+}
+
+template <class TT>
+__global__ void __launch_bounds__(kFThreads) conv_follow_tma_kernel(const MatchParams P,
+                                                                    const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const DevDfa& d = P.d;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    TT T;
+    T.init(d, stage_table<TT::kSmem, TT::kW32>(d, sm));
+    const size_t tb = smem_tab_bytes(d, TT::kSmem);
+    const uint32_t sraw = smem_u32(sm);
+    const uint32_t stg = (sraw + (uint32_t)tb + 1023u) & ~1023u;   // 1024-aligned staging (swizzle atoms)
+    const uint32_t stage0 = stg + warp * kFStages * kFStageBytes;
+    const uint32_t mbar0 = stg + nw * kFStages * kFStageBytes + warp * kFStages * 8u;
+    const ConvWs W = conv_ws(P);
+    const uint8_t* in = P.in;
+    const uint64_t pfull = P.p - 1;   // rows covered by the tensor map (the last chunk is not a full row)
+    const uint32_t nst = (uint32_t)(P.L / kFBox);
+    const uint64_t row0 = (uint64_t)blockIdx.x * blockDim.x + warp * 32u;
+    const uint64_t t = row0 + lane;
+
+    Follow<TT, 1> F(T);
+    F.bad = 0;
+    F.A = d.A;
+    F.check = d.A < 256;
+    F.wmask = T.word_mask();
+    F.K = ((256u - d.A) & 0xFFu) * 0x01010101u;
+    F.K7F = F.K & 0x7F7F7F7Fu;
+    const bool live = t < P.p;
+    const ConvChunk* info = W.info + (live ? t : 0);
+    const uint64_t b0 = conv_b(P, t), b1 = live ? conv_b(P, t + 1) : b0;
+    const uint32_t D0 = live ? info->D : 0u;
+    F.D[0] = D0 == kWide ? 0u : D0;   // follow only handed-over chunks
+    const bool act = F.D[0] != 0;
+    const uint32_t m = act ? info->m : 0u;
+#pragma unroll
+    for (int k = 0; k < (int)kDMax; ++k) {
+        F.e[0][k] = act ? T.start(info->z[k]) : 0u;
+        F.h[0][k] = 0;
+    }
+    const bool staged = act && t < pfull;
+    // first staged 16-byte unit of this row; bytes [m, 16 su) are walked from global memory
+    const uint32_t su = staged ? (m + 15u) >> 4 : 0xFFFFFFFFu;
+    uint32_t s_lo = su >> 2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s_lo = min(s_lo, __shfl_xor_sync(0xFFFFFFFFu, s_lo, o));
+    const bool warp_staged = s_lo < nst;
+    if (lane == 0 && warp_staged) {
+        for (uint32_t k = 0; k < kFStages; ++k) mbar_init(mbar0 + 8 * k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (uint32_t k = 0; k < kFStages && s_lo + k < nst; ++k) {
+            mbar_expect_tx(mbar0 + 8 * k, kFStageBytes);
+            tma_load_2d(stage0 + k * kFStageBytes, &tmap, (int32_t)((s_lo + k) * kFBox), (int32_t)row0, mbar0 + 8 * k);
+        }
+    }
+    __syncthreads();   // table staged, barriers initialised
+
+    if (staged) {
+        const uint64_t hb = b0 + min((uint64_t)su * 16u, b1 - b0);
+        for (uint64_t a = b0 + m; a < hb; ++a) F.step1(0, in[a]);
+    }
+    const uint32_t Dw = __reduce_max_sync(0xFFFFFFFFu, staged ? F.D[0] : 0u);
+    bool merged = Dw <= 1;
+    uint32_t e0 = 0, h0 = 0;
+    if (warp_staged) {
+        const uint32_t sw = (lane >> 1) & 3u, off = lane * kFBox;
+        uint32_t slot = 0, phase = 0;
+        for (uint32_t s = s_lo; s < nst; ++s) {
+            mbar_wait(mbar0 + 8 * slot, phase);
+            const uint32_t buf = stage0 + slot * kFStageBytes;
+            uint4 x[4];
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) x[u] = lds128(buf + off + ((u ^ sw) << 4));
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) {
+                if (4 * s + u < su) continue;   // before this row's first staged unit (or not staged)
+                if (merged) {
+                    F.template word<1>(0, x[u].x);
+                    F.template word<1>(0, x[u].y);
+                    F.template word<1>(0, x[u].z);
+                    F.template word<1>(0, x[u].w);
+                } else {
+                    F.template word<kDMax>(0, x[u].x);
+                    F.template word<kDMax>(0, x[u].y);
+                    F.template word<kDMax>(0, x[u].z);
+                    F.template word<kDMax>(0, x[u].w);
+                }
+            }
+            // refill this slot only after every lane consumed its staged words (the TMA
+            // write must not overtake an in-flight shared load of the same buffer)
+            __syncwarp();
+            if (lane == 0 && s + kFStages < nst) {
+                mbar_expect_tx(mbar0 + 8 * slot, kFStageBytes);
+                tma_load_2d(buf, &tmap, (int32_t)((s + kFStages) * kFBox), (int32_t)row0, mbar0 + 8 * slot);
+            }
+            if (++slot == kFStages) {
+                slot = 0;
+                phase ^= 1u;
+            }
+            if (!merged) {
+                bool conv = true;
+#pragma unroll
+                for (int k = 1; k < (int)kDMax; ++k)
+                    conv &= !staged || (uint32_t)k >= F.D[0] || T.state(F.e[0][k]) == T.state(F.e[0][0]);
+                if (__all_sync(0xFFFFFFFFu, conv)) {
+                    merged = true;
+                    e0 = F.e[0][0];
+                    h0 = F.h[0][0];
+                }
+            }
+        }
+        if (staged && Dw > 1 && merged) {   // rebuild the routes carried by route 0
+#pragma unroll
+            for (int k = 1; k < (int)kDMax; ++k)
+                if ((uint32_t)k < F.D[0]) {
+                    F.h[0][k] = F.h[0][0] + (F.h[0][k] - h0);   // u32 wrap-around is exact here
+                    F.e[0][k] = F.e[0][0];
+                }
+        }
+        (void)e0;
+    }
+    if (act && !staged) {   // the last chunk: from global memory, every route
+        for (uint64_t a = b0 + m; a < b1; ++a) F.step1(0, in[a]);
     }
     if (!act) return;
     SurvRec& sr = W.surv[t];
-    sr.n = D;
+    sr.n = F.D[0];
 #pragma unroll
     for (int k = 0; k < (int)kDMax; ++k)
-        if ((uint32_t)k < D) {
+        if ((uint32_t)k < F.D[0]) {
             sr.z[k] = info->z[k];
-            sr.end[k] = T.state(e[k]);
-            sr.tail[k] = h[k];
+            sr.end[k] = T.state(F.e[0][k]);
+            sr.tail[k] = F.h[0][k];
         }
-    if (bad) {
-        const uint64_t off = first_bad(in, b0 + info->m, b1, A);
+    if (F.bad & 0x80808080u) {
+        const uint64_t off = first_bad(in, b0 + m, b1, d.A);
         if (off < b1) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
     }
 }
@@ -899,37 +1184,78 @@ __global__ void __launch_bounds__(kFollowThreads) conv_resolve_kernel(const Matc
     write_result(P, h->final_q, h->hits, dead);
 }
 
+template <class TT, int CPT>
+cudaError_t launch_follow(const Plan& plan, const MatchParams& P, size_t smem, cudaStream_t s) {
+    const void* fn = reinterpret_cast<const void*>(&conv_follow_kernel<TT, CPT>);
+    cudaError_t e = smem_optin(fn, smem);
+    if (e != cudaSuccess) return e;
+    if (!TT::kSmem) {
+        // global (L2-resident) tables: give the unified L1/shared array to L1 (set once)
+        static std::once_flag once;
+        std::call_once(once, [fn]() { cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 0); });
+    }
+    const uint64_t per = (uint64_t)plan.conv_fthreads * CPT;
+    const unsigned g = (unsigned)((P.p + per - 1) / per);
+    conv_follow_kernel<TT, CPT><<<g, plan.conv_fthreads, smem, s>>>(P);
+    return cudaGetLastError();
+}
+
+// TMA-staged follow when the input is 16-byte aligned and rows are whole boxes; false =
+// not applicable (the caller uses the thread-stream follow)
+template <class TT>
+bool launch_follow_tma(const MatchParams& P, size_t tb, cudaStream_t s, cudaError_t* err) {
+    if ((((uintptr_t)P.in) & 15u) || P.L % kFBox || P.L < kFBox || P.p < 2) return false;
+    CUtensorMap map;
+    memset(&map, 0, sizeof(map));
+    if (!encode_rows_map(&map, P.in, P.L, P.p - 1, kFBox, 32)) return false;
+    const void* fn = reinterpret_cast<const void*>(&conv_follow_tma_kernel<TT>);
+    cudaError_t e = smem_optin(fn, follow_tma_smem(tb));
+    if (e == cudaSuccess) {
+        void* args[] = {const_cast<MatchParams*>(&P), &map};
+        const unsigned g = (unsigned)((P.p + kFThreads - 1) / kFThreads);
+        e = cudaLaunchKernel(fn, dim3(g), dim3(kFThreads), args, follow_tma_smem(tb), s);
+    }
+    *err = e;
+    return true;
+}
+
+template <class TT>
+cudaError_t launch_follow_cpt(const Plan& plan, const MatchParams& P, size_t smem, cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    if (plan.conv_tma && launch_follow_tma<TT>(P, smem, s, &e)) return e;
+    return plan.conv_cpt == 2 ? launch_follow<TT, 2>(plan, P, smem, s) : launch_follow<TT, 1>(plan, P, smem, s);
+}
+
 template <bool SMEM, bool W32>
 int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     const DevDfa& d = P.d;
     const size_t tb = smem_tab_bytes(d, SMEM);
-    const size_t s1 = tb + kSetWarps * set_warp_bytes(P.slots, d.Qpad);
-    cudaError_t e = cudaFuncSetAttribute(conv_set_kernel<SMEM, W32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(conv_follow_kernel<SMEM, W32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(conv_map_kernel<SMEM, W32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb);
-    if (!SMEM && e == cudaSuccess) {
-        // global (L2-resident) tables: give the unified L1/shared array to L1
-        cudaFuncSetAttribute(conv_follow_kernel<SMEM, W32>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-
-    }
-    if (e != cudaSuccess) {
-        set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-        return PAREM_ECUDA;
-    }
+    const uint32_t sw = kSetWarps;
+    const size_t s1 = tb + sw * set_warp_bytes(P.slots, d.Qpad);
+    const bool own = d.Qpad <= kOwnerMaxQ && P.set_own;
+    const void* setfn = own ? reinterpret_cast<const void*>(&conv_set_kernel<SMEM, W32, true>)
+                            : reinterpret_cast<const void*>(&conv_set_kernel<SMEM, W32, false>);
+    cudaError_t e = smem_optin(setfn, s1);
+    if (e == cudaSuccess) e = smem_optin(reinterpret_cast<const void*>(&conv_map_kernel<SMEM, W32>), tb);
     int bps = 0, sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, conv_set_kernel<SMEM, W32>, kSetWarps * 32, s1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, setfn, sw * 32, s1);
     if (bps < 1) bps = 1;
-    uint64_t g1w = (P.p + kSetWarps - 1) / kSetWarps;
+    uint64_t g1w = (P.p + sw - 1) / sw;
     const unsigned g1 = (unsigned)(g1w < (uint64_t)sms * bps ? g1w : (uint64_t)sms * bps);
     const unsigned g2 = (unsigned)((P.p + kFollowThreads - 1) / kFollowThreads);
-    conv_set_kernel<SMEM, W32><<<g1, kSetWarps * 32, s1, s>>>(P);
+    {
+        void* args[] = {const_cast<MatchParams*>(&P)};
+        e = cudaLaunchKernel(setfn, dim3(g1), dim3(sw * 32), args, s1, s);
+    }
     prof_after("conv_set", s);
-    conv_follow_kernel<SMEM, W32><<<g2, kFollowThreads, tb, s>>>(P);
+    e = launch_follow_cpt<Tab<SMEM, W32>>(plan, P, tb, s);
     prof_after("conv_follow", s);
+    if (e != cudaSuccess) {
+        set_error("conv_follow: %s", cudaGetErrorString(e));
+        return PAREM_ECUDA;
+    }
     conv_ends_kernel<<<g2, kFollowThreads, 0, s>>>(P);
     prof_after("conv_ends", s);
     conv_wide_kernel<W32><<<1, 32, 0, s>>>(P);
@@ -938,7 +1264,8 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     int bpm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, conv_map_kernel<SMEM, W32>, kSetWarps * 32, tb);
     if (bpm < 1) bpm = 1;
-    const unsigned gm = (unsigned)(g1w < (uint64_t)sms * bpm ? g1w : (uint64_t)sms * bpm);
+    const uint64_t gmw = (P.p + kSetWarps - 1) / kSetWarps;
+    const unsigned gm = (unsigned)(gmw < (uint64_t)sms * bpm ? gmw : (uint64_t)sms * bpm);
     conv_map1_kernel<W32><<<g2, kFollowThreads, 0, s>>>(P);
     prof_after("conv_map1", s);
     conv_map_kernel<SMEM, W32><<<gm, kSetWarps * 32, tb, s>>>(P);
@@ -968,8 +1295,8 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
 
 size_t conv_ws_total(uint64_t p) { return conv_ws_bytes(p); }
 
-size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap) {
-    return smem_tab_bytes(d, smem_tab) + kSetWarps * set_warp_bytes(cap, d.Qpad);
+size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap, uint32_t warps) {
+    return smem_tab_bytes(d, smem_tab) + warps * set_warp_bytes(cap, d.Qpad);
 }
 
 int launch_conv(const Plan& plan, const MatchParams& P, cudaStream_t s) {

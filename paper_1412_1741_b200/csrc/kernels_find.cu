@@ -342,7 +342,7 @@ int launch_find(const Plan& plan, const MatchParams& P, cudaStream_t s) {
                                                : (const void*)find_emit_lanes_kernel<true, false>)
                                        : (smem ? (const void*)find_emit_lanes_kernel<false, true>
                                                : (const void*)find_emit_lanes_kernel<false, false>);
-        if (smem) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (smem) smem_optin(fn, sm);
         void* args[] = {const_cast<MatchParams*>(&P)};
         cudaLaunchKernel(fn, dim3(nblk(p, kFindThreads)), dim3(kFindThreads), args, sm, s);
     }

@@ -285,7 +285,7 @@ size_t lanes_smem_bytes(const DevDfa& d, bool smem_tab) { return lanes_layout(d,
 int lanes_blocks_per_sm(uint32_t U, bool smem_tab, bool u32, uint32_t threads, size_t smem) {
     const void* fn = lanes_dispatch(U, smem_tab, u32);
     if (!fn) return 0;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_optin(fn, smem);
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, (int)threads, smem) != cudaSuccess) return 0;
     return nb;
@@ -297,7 +297,7 @@ int launch_lanes(const Plan& plan, const MatchParams& P, cudaStream_t s) {
         set_error("no lanes kernel for U=%u", plan.U);
         return PAREM_EINTERNAL;
     }
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
+    cudaError_t e = smem_optin(fn, plan.smem);
     if (e != cudaSuccess) {
         set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
         return PAREM_ECUDA;

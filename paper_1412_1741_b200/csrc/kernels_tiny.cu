@@ -69,6 +69,21 @@ EncodeFn encode_fn() {
 
 }  // namespace
 
+// A 2-D uint8 tensor map over rows of `row_len` bytes (row stride = row_len), box
+// box_w x box_rows, 64-byte swizzle (TMA row streaming: tiny kernel, converging follow).
+bool encode_rows_map(CUtensorMap* map, const uint8_t* base, uint64_t row_len, uint64_t rows, uint32_t box_w,
+                     uint32_t box_rows) {
+    EncodeFn enc = encode_fn();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)row_len, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)row_len};
+    const cuuint32_t box[2] = {box_w, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Register slots per chunk (routes advanced together).  Generic-alphabet kernels (B = 0:
 // one table lookup per symbol) are instantiated for fewer K to bound the build.
 uint32_t tiny_round_slots(uint32_t k, uint32_t B) {
@@ -113,7 +128,7 @@ uint32_t tiny_pick_stages(const DevDfa& d, uint32_t B) {
 int tiny_blocks_per_sm(uint32_t K, uint32_t B, bool tma, size_t smem) {
     const void* fn = tiny_dispatch(K, B, tma);
     if (!fn) return 0;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_optin(fn, smem);
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kT, smem) != cudaSuccess) return 0;
     return nb;
@@ -126,16 +141,7 @@ int launch_tiny(const Plan& plan, const MatchParams& P, cudaStream_t s) {
                P.p * P.L <= P.n;
     CUtensorMap map;
     memset(&map, 0, sizeof(map));
-    if (tma) {
-        EncodeFn enc = encode_fn();
-        const cuuint64_t dims[2] = {(cuuint64_t)P.L, (cuuint64_t)P.p};
-        const cuuint64_t strides[1] = {(cuuint64_t)P.L};
-        const cuuint32_t box[2] = {kBoxBytes, kRowsW};
-        const cuuint32_t estr[2] = {1, 1};
-        tma = enc && enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(P.in), dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-    }
+    if (tma) tma = encode_rows_map(&map, P.in, P.L, P.p, kBoxBytes, kRowsW);
     const void* fn = tiny_dispatch(plan.slots, P.d.sym_bits, tma);
     if (!fn) {
         set_error("no tiny kernel for K=%u B=%u", plan.slots, P.d.sym_bits);
@@ -144,7 +150,7 @@ int launch_tiny(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     MatchParams Q = P;
     Q.stages = tma ? plan.tma : 0u;
     const size_t smem = tiny_smem_bytes(P.d, P.d.sym_bits, Q.stages);
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = smem_optin(fn, smem);
     if (e != cudaSuccess) {
         set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
         return PAREM_ECUDA;

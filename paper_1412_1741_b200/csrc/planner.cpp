@@ -87,8 +87,9 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
     // enough for u16 candidate lists and the set walk's per-warp scratch
     const uint32_t conv_cap = cand == PAREM_CANDIDATES_ENUM ? d.Q : d.Lmax;
     const bool conv_smem_tab = d.lanes_tab && (size_t)d.Apad * d.Qpad * (d.lanes_u32 ? 4 : 2) <= (size_t)160 * 1024;
+    const uint32_t conv_swarps = 8;   // set-walk warps per CTA
     const bool conv_ok = d.lanes_tab && !d.has_sink && d.Qpad <= 65536 && dfa->conv_t4 > 0 &&
-                         conv_set_smem_bytes(d, conv_smem_tab, conv_cap) <= (size_t)200 * 1024;
+                         conv_set_smem_bytes(d, conv_smem_tab, conv_cap, conv_swarps) <= (size_t)200 * 1024;
     uint32_t kernel = kreq ? kreq
                            : (d.Qp <= kTinyMaxStates ? kKernelTiny : (conv_ok ? kKernelConv : kKernelLanes));
     if (kernel == kKernelConv && !conv_ok) {
@@ -157,28 +158,54 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
     }
 
     if (kernel == kKernelConv) {
-        // K2 runs one thread per chunk: aim for a full wave of them, but keep chunks long
-        // against the set walk's head (~conv_t4 symbols) so K1 stays a small share.
+        // K2 follows one dependent chain per chunk: the chunk count is the number of
+        // lookups in flight (~1024 per SM: 512-thread CTAs, two per SM); the set walk's cost
+        // grows with the chunk count, and chunks stay long against the walk's head (~conv_t4
+        // symbols).  The follow streams its rows through TMA boxes of 64 bytes, so planner
+        // row lengths are whole boxes (and not multiples of 256 B: TMA row streams at such
+        // strides are slower, profiles/r01_stride_probe.txt).
+        // Follow input: each thread streams its row with 16-byte loads that do not allocate
+        // in L1 (an L2-resident table keeps the whole L1: carveout 0).  The TMA-staged
+        // follow (conv_tma) is faster per byte on shared-memory tables but needs ~1024
+        // chains per SM; at that chunk count the set walk costs more than it saves (cfg3:
+        // 3.13 ms vs 2.95 ms per step, profiles/r02_conv_sweeps.txt), so it is opt-in.
+        plan->conv_tma = 0;
+        plan->set_own = 1;
+        if (const char* e = getenv("PAREM_CONV_TMA")) plan->conv_tma = (uint32_t)atoi(e);   // experiments
+        if (const char* e = getenv("PAREM_SET_OWN")) plan->set_own = (uint32_t)atoi(e);
+        plan->conv_fthreads = 512;
+        plan->conv_cpt = 1;
+        plan->conv_swarps = conv_swarps;
+        if (const char* e = getenv("PAREM_CONV_CPT")) plan->conv_cpt = atoi(e) == 2 ? 2 : 1;
         uint64_t L;
-        // K2 runs one thread per chunk; 512 per SM measured best on cfg3/cfg5 (fewer chunks =
-        // less set-walk work, enough chains to keep the lookups in flight)
-        uint64_t chains = (uint64_t)sms * 512;
+        // chains: 512 per SM -- one 512-thread follow CTA per SM, exactly one wave (a partial
+        // second wave or unevenly loaded SMs cost more than the extra chains bring); the
+        // follow is bound by shared-memory bank conflicts (smem tables) or L1TEX gather
+        // wavefronts (L2 tables), not by latency, and more chunks only add set-walk work
+        uint64_t chains = (uint64_t)sms * (plan->conv_tma ? 1024 : 512);
         uint32_t dmax = 4;
+        uint64_t headx = 16;
         if (const char* e = getenv("PAREM_CONV_CHAINS")) chains = strtoull(e, nullptr, 10);   // experiments
+        if (const char* e = getenv("PAREM_CONV_HEADX")) headx = strtoull(e, nullptr, 10);
         if (const char* e = getenv("PAREM_CONV_DMAX")) dmax = (uint32_t)atoi(e);
         if ((dmax != 1 && dmax != 2) || dfa->conv_t1 == 0) dmax = 4;
         if (forced) L = forced;
         else {
             L = ceil_div(n, chains ? chains : 1);
-            // chunks >= 16x the probe's convergence length, so open chunks (no hand-over,
-            // resolved by head walks in the join) stay rare
-            const uint64_t head = 16ull * (dmax == 4 ? dfa->conv_t4 : dfa->conv_t1);
+            // chunks >= headx times the probe's convergence length, so open chunks (no
+            // hand-over, resolved by head walks in the join) stay rare
+            const uint64_t head = headx * (dmax == 4 ? dfa->conv_t4 : dfa->conv_t1);
             if (L < head) L = head;
             if (L < 4096) L = 4096;
-            L = (L + 15) & ~15ull;
-            // thread-per-chunk 16-B load streams at a stride that is a multiple of 128 B run
-            // ~18% slower (profiles/r01_stride_probe.txt): shift such strides by 16 B
-            if (L % 128 == 0) L += 16;
+            if (plan->conv_tma) {
+                L = (L + 63) & ~63ull;
+                if (L % 256 == 0) L += 64;
+            } else {
+                L = (L + 15) & ~15ull;
+                // thread-per-chunk 16-B load streams at a stride that is a multiple of 128 B
+                // run ~18% slower (profiles/r01_stride_probe.txt): shift such strides by 16 B
+                if (L % 128 == 0) L += 16;
+            }
         }
         if (L > (1ull << 30)) L = 1ull << 30;
         // planner-chosen lengths: the remainder forms a SHORTER last chunk (p = ceil(n / L)),
@@ -195,7 +222,7 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         plan->sym_per_lookup = 1;
         plan->win = 0;
         plan->smem_tab = conv_smem_tab;
-        plan->smem = conv_set_smem_bytes(d, conv_smem_tab, conv_cap);
+        plan->smem = conv_set_smem_bytes(d, conv_smem_tab, conv_cap, conv_swarps);
         plan->off_maps = 256;
         plan->off_hits = 0;
         plan->ws = al256(plan->off_maps + conv_ws_total(p));

@@ -64,6 +64,16 @@ def test_create_rejects_bad_arguments(L, table, start, why):
     assert L.parem_last_error()
 
 
+def test_create_rejects_too_many_states(L):
+    # u32 device offsets: Q > 2^22 is refused before the table is read
+    t = np.zeros(4, np.uint32)
+    bm = np.zeros(1, np.uint8)
+    h = C.c_void_p()
+    rc = L.parem_dfa_create((1 << 22) + 1, 1, t.ctypes.data, 4, 0, bm.ctypes.data, C.byref(h))
+    assert rc == -1 and not h.value
+    assert b"4194304" in L.parem_last_error()
+
+
 def test_null_handles(L):
     assert L.parem_dfa_destroy(None) == 0
     assert L.parem_workspace_bytes(None, 10, None) == 0
