@@ -530,7 +530,39 @@ def run_config(k: int, args, dist, rank: int, ws_: int, dev, micro: Micro, headl
                                       "bytes_per_buffer": n, "ms_per_graph": round(gms, 4),
                                       "us_per_match": round(1e3 * gms / K, 3),
                                       "note": "CUDA graph of K serialised matches over K distinct buffers"}
-            del bufs, graph
+            del graph
+            # the batched entry (parem_match_batch_async): all K inputs in ONE launch -- the
+            # number compared with the 50 % bar for small inputs (SURVEY §8(d) note 1)
+            bws = torch.zeros(dfa.batch_workspace_bytes(n, K, opts), dtype=torch.uint8, device=dev)
+            bres = torch.zeros(56 * K, dtype=torch.uint8, device=dev)
+            for _ in range(3):
+                dfa.match_batch_async(bufs, bws, bres, opts, stream)
+            torch.cuda.synchronize()
+            breps = 10
+            P.profile(True)
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record(stream)
+            for _ in range(breps):
+                dfa.match_batch_async(bufs, bws, bres, opts, stream)
+            b1.record(stream)
+            torch.cuda.synchronize()
+            P.profile(False)
+            bk = kernel_medians(P.profile_read())[0]
+            bms = reduce_max(b0.elapsed_time(b1) / breps, dist, dev)
+            bb = bres.cpu().numpy().tobytes()
+            last = P.MatchResult.from_bytes(bb[56 * (K - 1): 56 * K])
+            ref_last = P.MatchResult.from_bytes(res.cpu().numpy().tobytes()[:56])   # graph's last match = input K-1
+            assert (last.final_state, last.match_count) == (ref_last.final_state, ref_last.match_count)
+            bval = K * n * ws_ / (bms * 1e-3) / 1e9
+            hbm_peak = peaks()[0]
+            entry["batched"] = {"value": round(bval, 1), "unit": UNIT, "inputs": K, "bytes_per_input": n,
+                                "ms_per_batch": round(bms, 4), "us_per_match": round(1e3 * bms / K, 3),
+                                "launches_per_batch": len(bk) and 1, "kernels_ms": {kk: round(v, 4) for kk, v in bk.items()},
+                                "roofline": {"bound": "hbm", "achieved": round(bval / ws_, 1), "peak": hbm_peak,
+                                             "frac": round(bval / ws_ / hbm_peak, 4)},
+                                "note": "parem_match_batch_async: K independent matches in one launch; "
+                                        "the small-input number compared with the 50 % bar"}
+            del bufs, bws, bres
 
     # ---- NEXT-1: the paper's comparison, PaREM vs Enumeration ----
     if not args.no_enum and args.candidates == "parem":

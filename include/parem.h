@@ -132,6 +132,21 @@ size_t parem_workspace_bytes(const parem_dfa* dfa, uint64_t n, const parem_optio
 int parem_match_async(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, void* d_ws, size_t ws_bytes,
                       const parem_options* opts, parem_result* d_result, void* stream /* cudaStream_t */);
 
+/* Batched matching: `count` INDEPENDENT inputs of n bytes each, laid out back to back at
+ * d_input (input i = d_input[i*n .. (i+1)*n)), each matched from q0 exactly as
+ * parem_match_async would (the paper's method per input: P:65-70), results to
+ * d_results[0 .. count) (device, caller-owned).  When every input is a whole number of
+ * the tiny kernel's 1024-chunk tiles (DFAs with <= 32 internal states, n a multiple of
+ * 64 KiB, 16-byte aligned input, no SNAP/look-back options) all inputs run in ONE launch
+ * -- the throughput path for many small inputs (packets, reads): a single 1 MiB match is
+ * launch- and drain-bound.  Otherwise the inputs are matched one after another on the
+ * stream (same workspace).  Workspace: parem_batch_workspace_bytes(dfa, n, count, opts).
+ * Per-input status/bad_offset as in parem_match_async (offsets local to the input). */
+size_t parem_batch_workspace_bytes(const parem_dfa* dfa, uint64_t n, uint64_t count, const parem_options* opts);
+int parem_match_batch_async(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, uint64_t count, void* d_ws,
+                            size_t ws_bytes, const parem_options* opts, parem_result* d_results,
+                            void* stream /* cudaStream_t */);
+
 /* Like parem_match_async, but the walk continues from a previous segment's result:
  * the start state is d_carry->final_state (PAREM_DEAD stays dead), counts add to
  * d_carry->match_count and bad offsets are reported as offset_base + local offset

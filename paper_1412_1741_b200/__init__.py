@@ -243,6 +243,38 @@ class Dfa:
         if st != PAREM_OK:
             _err(self._L, st)
 
+    def batch_workspace_bytes(self, n: int, count: int, opts=None) -> int:
+        ws = self._L.parem_batch_workspace_bytes(self._h, n, count, C.byref(opts) if opts is not None else None)
+        if ws == 0:
+            _err(self._L, PAREM_EINVAL)
+        return ws
+
+    def match_batch_async(self, x, ws, results, opts=None, stream=None) -> None:
+        """Enqueue parem_match_batch_async: ``x`` is a CUDA uint8 tensor of shape (count, n)
+        (count independent inputs, contiguous); ``results`` a CUDA uint8 tensor of at least
+        56 * count bytes receiving one parem_result per input."""
+        x = _cuda_u8(x)
+        if x.dim() != 2:
+            raise TypeError("batch input must be a 2-D (count, n) tensor")
+        count, n = x.shape
+        st = self._L.parem_match_batch_async(self._h, C.c_void_p(x.data_ptr()), n, count, C.c_void_p(ws.data_ptr()),
+                                             ws.numel(), C.byref(opts) if opts is not None else None,
+                                             C.c_void_p(results.data_ptr()), _stream(stream))
+        if st != PAREM_OK:
+            _err(self._L, st)
+
+    def match_batch(self, x, opts=None) -> list:
+        """Synchronous batched match of a (count, n) CUDA uint8 tensor: one MatchResult per row."""
+        import torch
+
+        x = _cuda_u8(x)
+        count, n = x.shape
+        ws = torch.zeros(self.batch_workspace_bytes(n, count, opts), dtype=torch.uint8, device=x.device)
+        res = torch.zeros(max(1, count) * 56, dtype=torch.uint8, device=x.device)
+        self.match_batch_async(x, ws, res, opts)
+        b = res.cpu().numpy().tobytes()
+        return [MatchResult.from_bytes(b[56 * i: 56 * (i + 1)]) for i in range(count)]
+
     def find_workspace_bytes(self, n: int, opts=None) -> int:
         ws = self._L.parem_find_workspace_bytes(self._h, n, C.byref(opts) if opts is not None else None)
         if ws == 0:

@@ -62,6 +62,7 @@ EXPORTS = [
     "parem_match_continue_async", "parem_match", "parem_match_host", "parem_dfa_get_info", "parem_plan",
     "parem_last_error", "parem_version", "parem_bench_read_stream", "parem_bench_gather", "parem_profile",
     "parem_profile_read", "parem_regex_compile", "parem_find_async", "parem_find_workspace_bytes",
+    "parem_batch_workspace_bytes", "parem_match_batch_async",
 ]
 
 _LIB = None
@@ -88,6 +89,10 @@ def load(path: str = SO_PATH):
     L.parem_match_async.argtypes = [vp, vp, u64, vp, sz, O, vp, vp]
     L.parem_match_continue_async.restype = i32
     L.parem_match_continue_async.argtypes = [vp, vp, u64, u64, vp, sz, O, vp, vp, vp]
+    L.parem_batch_workspace_bytes.restype = sz
+    L.parem_batch_workspace_bytes.argtypes = [vp, u64, u64, O]
+    L.parem_match_batch_async.restype = i32
+    L.parem_match_batch_async.argtypes = [vp, vp, u64, u64, vp, sz, O, vp, vp]
     L.parem_match.restype = i32
     L.parem_match.argtypes = [vp, vp, u64, O, R, vp]
     L.parem_match_host.restype = i32

@@ -202,6 +202,100 @@ extern "C" int parem_match_async(const parem_dfa* dfa, const uint8_t* d_input, u
     return match_impl(dfa, d_input, n, 0, d_ws, ws_bytes, opts, nullptr, d_result, (cudaStream_t)stream);
 }
 
+// ---- batched matching: many independent inputs in one launch (tiny kernel) ----
+namespace parem {
+namespace {
+// Batch plan: the tiny kernel with every input an exact multiple of its 1024-chunk CTA tile
+// (chunk length a multiple of the 64-byte TMA box), so no warp or CTA spans two inputs.
+// Returns false if the batch cannot run as one launch (the caller loops over the inputs).
+bool batch_plan(const parem_dfa* dfa, uint64_t n, uint64_t count, const parem_options* opts, Plan* plan,
+                uint64_t* cpi) {
+    if (!dfa || n == 0 || count == 0) return false;
+    if (opts && (opts->candidates == PAREM_CANDIDATES_LOOKBACK || opts->boundary_policy == PAREM_BOUNDARY_SNAP ||
+                 (opts->kernel && opts->kernel != kKernelTiny)))
+        return false;
+    if (make_plan(dfa, n, opts, plan) != PAREM_OK || plan->kernel != kKernelTiny || !plan->tma) return false;
+    const uint64_t rows = (uint64_t)kTinyThreads * kTinyRowsPerThread;   // chunks per CTA tile
+    const int sms = dfa->num_sms > 0 ? dfa->num_sms : 148;
+    uint64_t bestL = 0, best = ~0ull;
+    for (uint64_t L = 64; L <= 4096; L *= 2) {
+        if (opts && opts->chunk_len && opts->chunk_len != L) continue;
+        if (n % (rows * L)) continue;
+        const uint64_t ctas = count * (n / (rows * L));
+        const uint64_t waves = (ctas + sms - 1) / sms;
+        const uint64_t cost = waves * (L / 64 + 2);   // ~2 box-times of fixed cost per CTA
+        if (cost < best) { best = cost; bestL = L; }
+    }
+    if (!bestL) return false;
+    *cpi = n / bestL;
+    const uint64_t ctas = count * (n / (rows * bestL));
+    if (ctas > 0x7FFFFFFFull) return false;
+    plan->L = bestL;
+    plan->p = count * *cpi;
+    plan->grid = ctas;
+    plan->policy = PAREM_BOUNDARY_GRID;
+    plan->win = 0;
+    plan->off_maps = 256 + ((count * 32 + 255) & ~255ull);
+    plan->ws = ((plan->off_maps + ctas * dfa->dev.Qpad * 8) + 255) & ~(size_t)255;
+    return true;
+}
+}  // namespace
+}  // namespace parem
+
+extern "C" size_t parem_batch_workspace_bytes(const parem_dfa* dfa, uint64_t n, uint64_t count,
+                                              const parem_options* opts) {
+    Plan plan;
+    uint64_t cpi = 0;
+    const size_t one = parem_workspace_bytes(dfa, n, opts);
+    if (!one) return 0;
+    if (batch_plan(dfa, n, count, opts, &plan, &cpi)) return plan.ws > one ? plan.ws : one;
+    return one;
+}
+
+extern "C" int parem_match_batch_async(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, uint64_t count,
+                                       void* d_ws, size_t ws_bytes, const parem_options* opts,
+                                       parem_result* d_results, void* stream_) {
+    set_error("");
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (!dfa || !d_results || (count && n && !d_input)) { set_error("null argument"); return PAREM_EINVAL; }
+    if (count == 0) return PAREM_OK;
+    if (!d_ws || (reinterpret_cast<uintptr_t>(d_ws) & 15)) { set_error("null or unaligned (16 B) workspace"); return PAREM_EINVAL; }
+    if (reinterpret_cast<uintptr_t>(d_results) & 7) { set_error("results must be 8-byte aligned"); return PAREM_EINVAL; }
+    Plan plan;
+    uint64_t cpi = 0;
+    if (!(((uintptr_t)d_input) & 15) && batch_plan(dfa, n, count, opts, &plan, &cpi)) {
+        if (ws_bytes < plan.ws) { set_error("workspace too small: %zu < %zu", ws_bytes, plan.ws); return PAREM_ENOMEM; }
+        MatchParams P;
+        memset(&P, 0, sizeof(P));
+        P.d = dfa->dev;
+        P.in = d_input;
+        P.n = n * count;
+        P.L = plan.L;
+        P.p = plan.p;
+        P.policy = PAREM_BOUNDARY_GRID;
+        P.cand = plan.cand;
+        P.slots = plan.slots;
+        P.hdr = reinterpret_cast<WsHeader*>(d_ws);
+        P.bstats = reinterpret_cast<unsigned long long*>(static_cast<char*>(d_ws) + 256);
+        P.maps = static_cast<char*>(d_ws) + plan.off_maps;
+        P.cpi = cpi;
+        P.n_one = n;
+        P.results = d_results;
+        if (!(opts && (opts->flags & PAREM_FLAG_WS_CLEAN))) {
+            cudaError_t e = cudaMemsetAsync(d_ws, 0, plan.off_maps, stream);
+            if (e != cudaSuccess) { set_error("cudaMemsetAsync: %s", cudaGetErrorString(e)); return PAREM_ECUDA; }
+        }
+        prof_begin(stream);
+        return launch_tiny(plan, P, stream);
+    }
+    // general case: one match per input, in order on the stream (they share the workspace)
+    for (uint64_t i = 0; i < count; ++i) {
+        const int rc = match_impl(dfa, d_input + i * n, n, 0, d_ws, ws_bytes, opts, nullptr, d_results + i, stream);
+        if (rc != PAREM_OK) return rc;
+    }
+    return PAREM_OK;
+}
+
 extern "C" int parem_match_continue_async(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n,
                                           uint64_t offset_base, void* d_ws, size_t ws_bytes,
                                           const parem_options* opts, const parem_result* d_carry,

@@ -71,6 +71,12 @@ struct MatchParams {
     uint32_t lookback;         // tiny: k of the look-back candidate rule
     uint32_t conv_cpt;         // conv: chunks per follow thread
     uint32_t set_own;          // conv: phase-A dedup by owner tags (else image bitmap + atomics)
+    // parem_match_batch_async (tiny kernel): `batch` independent inputs of n_one bytes laid
+    // out back to back; chunk t belongs to input t / cpi (cpi = a multiple of the CTA tile)
+    uint64_t cpi;              // chunks per input (0 = not a batch)
+    uint64_t n_one;            // bytes per input
+    parem_result* results;     // [batch] per-input results
+    unsigned long long* bstats;  // [batch][4]: ~bad offset (local), routes, steps, pad
     uint64_t offset_base;
     const parem_result* carry; // may be null
     parem_result* result;

@@ -200,7 +200,7 @@ __device__ __forceinline__ TinyChunk tiny_chunk(const MatchParams& P, uint64_t t
     if (c.live) {
         c.b0 = boundary_of(P, t, Lcnt);
         c.b1 = boundary_of(P, t + 1, Lcnt);
-        if (t == 0) {
+        if (t == 0 || (P.cpi && t % P.cpi == 0)) {   // first chunk (of every batch input)
             bool dead;
             c.q0 = start_state(P, &dead);
             c.cnt = 1;
@@ -282,8 +282,9 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
     for (int j = 0; j < K; ++j) {
         const uint32_t ka = ca.cnt ? min((uint32_t)j, ca.cnt - 1) : 0;
         const uint32_t kb = cb.cnt ? min((uint32_t)j, cb.cnt - 1) : 0;
-        const uint32_t sa = ca.t == 0 ? ca.q0 : (ca.cnt ? tiny_cand(ca, Llist, ka) : 0u);
-        const uint32_t sb = cb.cnt ? tiny_cand(cb, Llist, kb) : 0u;
+        const bool sta = ca.t == 0 || (P.cpi && ca.t % P.cpi == 0), stb = P.cpi && cb.t % P.cpi == 0;
+        const uint32_t sa = sta ? ca.q0 : (ca.cnt ? tiny_cand(ca, Llist, ka) : 0u);
+        const uint32_t sb = stb ? cb.q0 : (cb.cnt ? tiny_cand(cb, Llist, kb) : 0u);
         ra.e[j] = B ? ((sa << 11) | lane4) : sa;
         rb.e[j] = B ? ((sb << 11) | lane4) : sb;
         ra.h[j] = rb.h[j] = 0;
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
 #pragma unroll
         for (int j = 0; j < K; ++j)
             if ((uint32_t)j < c.cnt) {
-                const uint32_t s = c.t == 0 ? c.q0 : tiny_cand(c, Llist, j);
+                const uint32_t s = (c.t == 0 || (P.cpi && c.t % P.cpi == 0)) ? c.q0 : tiny_cand(c, Llist, j);
                 mend[lr * Qpad + s] = (uint8_t)r.state(j);
                 mhits[lr * Qpad + s] = r.h[j];
             }
@@ -440,7 +441,10 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
         if (c.cnt == 0 && first_bad(P.in, c.b0, c.b1, A) < c.b1) badacc = 1;   // R_i empty: still validate
         if (badacc) {
             const uint64_t off = first_bad(P.in, c.b0, c.b1, A);
-            if (off < c.b1) atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
+            if (off < c.b1) {
+                if (P.cpi) atomicMax(P.bstats + 4 * (c.t / P.cpi), ~(unsigned long long)(off - (c.t / P.cpi) * P.n_one));
+                else atomicMax(&P.hdr->bad_inv, ~(unsigned long long)off);
+            }
         }
     };
     // ---- A4 (first level): each warp composes its 64 chunk maps in row order, lane q =
@@ -472,8 +476,10 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
         const unsigned long long ss = warp_sum((ca.live ? (unsigned long long)ca.rc * (ca.b1 - ca.b0) : 0ull) +
                                                (cb.live ? (unsigned long long)cb.rc * (cb.b1 - cb.b0) : 0ull));
         if (lane == 0 && rs) {
-            atomicAdd(&P.hdr->routes, (unsigned long long)rs);
-            atomicAdd(&P.hdr->steps, ss);
+            // a warp's 64 chunks never span two batch inputs (inputs are whole CTA tiles)
+            unsigned long long* st = P.cpi ? P.bstats + 4 * (row0 / P.cpi) + 1 : &P.hdr->routes;
+            atomicAdd(st, (unsigned long long)rs);
+            atomicAdd(st + 1, ss);
         }
     }
     __syncthreads();
@@ -500,6 +506,45 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
     if (!*flag) return;
     __threadfence();
 
+    if (P.cpi) {   // batch: one fold per input, warp w takes inputs w, w + 16, ...
+        const uint32_t tpi = (uint32_t)(P.cpi / kRows);   // CTA tiles per input
+        const uint32_t nin = gridDim.x / tpi;
+        for (uint32_t b = warp; b < nin; b += kWarps) {
+            uint32_t ce = lane < Qpad ? lane : 0;
+            unsigned long long ch = 0;
+            for (uint32_t i = 0; i < tpi; ++i) {
+                const unsigned long long m =
+                    lane < Qpad ? ld_cg_u64(tiles + (uint64_t)(b * tpi + i) * Qpad + lane) : (unsigned long long)lane;
+                const uint32_t ne = __shfl_sync(0xFFFFFFFFu, (uint32_t)(m & 0xFFu), ce);
+                const unsigned long long nh = __shfl_sync(0xFFFFFFFFu, m >> 8, ce);
+                ch += nh;
+                ce = ne;
+            }
+            bool dead;
+            const uint32_t q0 = start_state(P, &dead);
+            const uint32_t qf = __shfl_sync(0xFFFFFFFFu, ce, q0);
+            const unsigned long long hf = __shfl_sync(0xFFFFFFFFu, ch, q0);
+            if (lane == 0) {
+                unsigned long long* st = P.bstats + 4 * b;
+                const bool sdead = P.d.has_sink && qf == P.d.sink;
+                parem_result r;
+                r.final_state = sdead ? PAREM_DEAD : qf;
+                r.accepted = sdead ? 0u : (uint32_t)P.d.acc[qf];
+                r.match_count = hf;
+                r.num_chunks = P.cpi;
+                r.routes = st[1];
+                r.route_steps = st[2];
+                r.reserved = 0;
+                r.status = st[0] ? PAREM_ESYMBOL : PAREM_OK;
+                r.bad_offset = st[0] ? ~st[0] : 0ull;
+                P.results[b] = r;
+                st[0] = st[1] = st[2] = 0ull;   // leave the workspace clean (PAREM_FLAG_WS_CLEAN)
+            }
+        }
+        __syncthreads();
+        if (tid == 0) reset_header(P);
+        return;
+    }
     // ---- last CTA: fold the tile maps along q0's path (lane q = start q, shuffles) ----
     const uint32_t G = gridDim.x;
     const uint32_t per = (G + kWarps - 1) / kWarps;
