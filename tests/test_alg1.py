@@ -82,6 +82,31 @@ def test_calculation_counts():
     assert oracle.route_stats(Tt, sym(EXAMPLE), [0, 6, 12, 18, 24]) == (6, 36)
 
 
+def test_enum_hidden_table():
+    """The hidden Enum table: all 28 routes of the General Enumeration
+    Approach on the worked example, visited state by visited state; the two rows the paper
+    misprints (reading C18) are checked against Table I directly."""
+    Tt = table1()
+    en = alg1.run_parem(Tt, 0, {8}, sym(EXAMPLE), 4, enum=True)
+    rows = [ln.split() for ln in open(os.path.join(GOLD, "table_enum_hidden.txt"))
+            if ln.strip() and not ln.startswith("#")]
+    assert len(rows) == 28 == en.calculations                       # "28 calculations" (P:431)
+    assert en.R == [[0]] + [list(range(9))] * 3
+    typos = 0
+    for r in rows:
+        i, start, printed = int(r[0][1:]), int(r[1]), [int(x) for x in r[2:8]]
+        got = en.routes[i][start].visited
+        if r[-1] == "typo":
+            typos += 1
+            assert got[1:] == printed[1:] and printed[0] == 8
+            assert got[0] == Tt[start][SIGMA.index("l")] == 0     # Table I: delta(2|3, l) = 0
+        else:
+            assert got == printed, r
+    assert typos == 2
+    # every route of P2 from a start other than 7 misses the match that 7 -> 8 makes
+    assert [s for s in range(9) if en.routes[2][s].hits] == [7]
+
+
 def test_compose_pins():
     """compose(P0, P1) maps 0 -> (7, 0); identity of an empty segment."""
     Tt = table1()
