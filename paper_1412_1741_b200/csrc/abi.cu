@@ -325,35 +325,66 @@ extern "C" int parem_match(const parem_dfa* dfa, const uint8_t* d_input, uint64_
     return h_result->status;
 }
 
+// Per-thread, per-device resources of parem_match_host: the copy stream and its events are
+// created once and reused (creating a stream and five events per call cost more than a
+// small match).  Deliberately never destroyed (process lifetime; the driver reclaims them).
+namespace parem {
+namespace {
+struct HostPipe {
+    int dev = -1;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t copied[2] = {nullptr, nullptr}, used[2] = {nullptr, nullptr}, ready = nullptr;
+};
+cudaError_t host_pipe(HostPipe** out) {
+    static thread_local HostPipe pipes[8];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    HostPipe& h = pipes[dev & 7];
+    if (h.dev != dev) {
+        e = cudaStreamCreateWithFlags(&h.cs, cudaStreamNonBlocking);
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+            e = cudaEventCreateWithFlags(&h.copied[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h.used[i], cudaEventDisableTiming);
+        }
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h.ready, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+        h.dev = dev;
+    }
+    *out = &h;
+    return cudaSuccess;
+}
+}  // namespace
+}  // namespace parem
+
 extern "C" int parem_match_host(const parem_dfa* dfa, const uint8_t* h_input, uint64_t n, const parem_options* opts,
                                 parem_result* h_result, void* stream_) {
     if (!h_result || !dfa || (n && !h_input)) { set_error("null argument"); return PAREM_EINVAL; }
     cudaStream_t stream = (cudaStream_t)stream_;
-    const uint64_t SEG = 64ull << 20;
+    // segments: 64 MiB for the tiny kernel; 512 MiB for the large-DFA paths, whose per-match
+    // cost has a part that scales with the chunk count rather than the bytes
+    Plan probe;
+    uint64_t SEG = 64ull << 20;
+    if (n > SEG && make_plan(dfa, SEG, opts, &probe) == PAREM_OK && probe.kernel != kKernelTiny) SEG = 512ull << 20;
     const uint64_t seg = n < SEG ? (n ? n : 1) : SEG;
     const size_t ws = parem_workspace_bytes(dfa, seg, opts);
     if (!ws) return PAREM_EINVAL;
     const size_t seg_al = (seg + 255) & ~(size_t)255, ws_al = (ws + 255) & ~(size_t)255;
     const size_t bytes = 2 * seg_al + ws_al + 256;
+    HostPipe* hp = nullptr;
+    cudaError_t e = host_pipe(&hp);
+    if (e != cudaSuccess) { set_error("stream setup: %s", cudaGetErrorString(e)); return PAREM_ECUDA; }
     void* blk = nullptr;
-    cudaError_t e = cudaMallocAsync(&blk, bytes, stream);
+    e = cudaMallocAsync(&blk, bytes, stream);
     if (e != cudaSuccess) { set_error("cudaMallocAsync: %s", cudaGetErrorString(e)); return PAREM_ENOMEM; }
     uint8_t* buf[2] = {static_cast<uint8_t*>(blk), static_cast<uint8_t*>(blk) + seg_al};
     void* d_ws = static_cast<uint8_t*>(blk) + 2 * seg_al;
     parem_result* d_res = reinterpret_cast<parem_result*>(static_cast<uint8_t*>(blk) + 2 * seg_al + ws_al);
-    cudaStream_t cs = nullptr;
-    cudaEvent_t copied[2] = {nullptr, nullptr}, used[2] = {nullptr, nullptr};
+    cudaStream_t cs = hp->cs;
     int rc = PAREM_OK;
-    e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
-        e = cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&used[i], cudaEventDisableTiming);
-    }
     // the copy stream must not start before the buffers exist on `stream`
-    cudaEvent_t ready = nullptr;
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventRecord(ready, stream);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ready, 0);
+    e = cudaEventRecord(hp->ready, stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, hp->ready, 0);
     if (e != cudaSuccess) {
         set_error("stream setup: %s", cudaGetErrorString(e));
         rc = PAREM_ECUDA;
@@ -363,13 +394,13 @@ extern "C" int parem_match_host(const parem_dfa* dfa, const uint8_t* h_input, ui
     for (uint64_t off = 0; rc == PAREM_OK && off < n; off += seg, ++k) {
         const uint64_t len = n - off < seg ? n - off : seg;
         const int b = (int)(k & 1);
-        if (k >= 2) cudaStreamWaitEvent(cs, used[b], 0);
+        if (k >= 2) cudaStreamWaitEvent(cs, hp->used[b], 0);
         e = cudaMemcpyAsync(buf[b], h_input + off, len, cudaMemcpyHostToDevice, cs);
-        if (e == cudaSuccess) e = cudaEventRecord(copied[b], cs);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, copied[b], 0);
+        if (e == cudaSuccess) e = cudaEventRecord(hp->copied[b], cs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, hp->copied[b], 0);
         if (e != cudaSuccess) { set_error("H2D: %s", cudaGetErrorString(e)); rc = PAREM_ECUDA; break; }
         rc = match_impl(dfa, buf[b], len, off, d_ws, ws, opts, off ? d_res : nullptr, d_res, stream);
-        if (rc == PAREM_OK && cudaEventRecord(used[b], stream) != cudaSuccess) rc = PAREM_ECUDA;
+        if (rc == PAREM_OK && cudaEventRecord(hp->used[b], stream) != cudaSuccess) rc = PAREM_ECUDA;
     }
     if (rc == PAREM_OK) {
         e = cudaMemcpyAsync(h_result, d_res, sizeof(parem_result), cudaMemcpyDeviceToHost, stream);
@@ -380,12 +411,6 @@ extern "C" int parem_match_host(const parem_dfa* dfa, const uint8_t* h_input, ui
     }
     cudaStreamSynchronize(cs);
     cudaFreeAsync(blk, stream);
-    for (int i = 0; i < 2; ++i) {
-        if (copied[i]) cudaEventDestroy(copied[i]);
-        if (used[i]) cudaEventDestroy(used[i]);
-    }
-    if (ready) cudaEventDestroy(ready);
-    if (cs) cudaStreamDestroy(cs);
     if (rc != PAREM_OK) return rc;
     return h_result->status;
 }

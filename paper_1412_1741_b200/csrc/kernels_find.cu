@@ -197,10 +197,9 @@ __global__ void __launch_bounds__(kFindThreads) find_emit_tiny_kernel(const Matc
     auto step = [&](uint32_t c, uint64_t k) {
         const uint32_t e = tab[s * A + (c < A ? c : A - 1)];
         s = e & 0x7FFFu;
-        if (e >> 15) {
-            if (o < P.fmax) P.fout[o] = k;
-            ++o;
-        }
+        const uint32_t h = e >> 15;   // predicated store (see find_emit_lanes_kernel)
+        if (h && o < P.fmax) P.fout[o] = k;
+        o += h;
     };
     uint64_t a = b0;
     for (; a < b1 && (((uintptr_t)(P.in + a)) & 15u); ++a) step(P.in[a], a);
@@ -215,6 +214,197 @@ __global__ void __launch_bounds__(kFindThreads) find_emit_tiny_kernel(const Matc
             for (uint32_t k = 0; k < 4; ++k) step(__byte_perm(w4[q], 0u, 0x4440u | k), a + 4 * q + k);
     }
     for (; a < b1; ++a) step(P.in[a], a);
+}
+
+// tiny tables with a stride table (A <= 4: B = 1 or 2 bits per symbol): one lookup per 4 / B
+// symbols, the tiny kernel's lane-replicated layout (entry = dest << 11 | lane << 2 |
+// hits << 28, lane l reads bank l).  A group with hits > 0 (rare for a search automaton) is
+// re-walked symbol by symbol through tab1 to emit its positions.  ~1 LOP3 + 1 LDS per group
+// instead of ~7 ops per symbol: the emit pass streams its chunk at close to the load rate.
+template <int B>
+__global__ void __launch_bounds__(kFindThreads) find_emit_stride_kernel(const MatchParams P) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const DevDfa& d = P.d;
+    const uint32_t lane = threadIdx.x & 31u;
+    uint32_t* tabk32 = reinterpret_cast<uint32_t*>(sm);
+    uint16_t* tab1 = reinterpret_cast<uint16_t*>(sm + (size_t)d.Qp * 2048);
+    for (uint32_t i = threadIdx.x; i < d.Qp * 512u; i += blockDim.x) tabk32[i] = __ldg(d.stride + (i >> 5)) | ((i & 31u) << 2);
+    for (uint32_t i = threadIdx.x; i < d.Qp * d.A; i += blockDim.x) tab1[i] = __ldg(d.tab1 + i);
+    __syncthreads();
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= P.p) return;
+    const unsigned char* tabk = sm;
+    const uint64_t b0 = find_b(P, t), b1 = find_b(P, t + 1);
+    const uint32_t A = d.A, lane4 = lane << 2;
+    uint32_t s = P.fchunk_q[t];
+    unsigned long long o = P.fchunk_base[t];
+    auto emit = [&](uint64_t k) {
+        if (o < P.fmax) P.fout[o] = k;
+        ++o;
+    };
+    auto step1 = [&](uint32_t c, uint64_t k) {
+        const uint32_t e = tab1[s * A + (c < A ? c : A - 1)];
+        s = e & 0x7FFFu;
+        if (e >> 15) emit(k);
+    };
+    uint64_t a = b0;
+    for (; a < b1 && (((uintptr_t)(P.in + a)) & 15u); ++a) step1(P.in[a], a);
+    uint32_t e = (s << 11) | lane4;
+    // one stride group: symbols (first, first + 1, ...) of word w, packed index g7
+    auto group = [&](uint32_t g7, uint32_t w, uint32_t first, uint64_t pos) {
+        const uint32_t prev = e;
+        e = *reinterpret_cast<const uint32_t*>(tabk + ((e & 0xFFFFu) | g7));
+        if (e >> 28) {   // rare: emit this group's positions symbol by symbol
+            s = (prev & 0xFFFFu) >> 11;
+#pragma unroll
+            for (uint32_t j = 0; j < 4u / B; ++j) step1((w >> (8 * (first + j))) & 0xFFu, pos + j);
+        }
+    };
+    auto word = [&](uint32_t w, uint64_t pos) {
+        if constexpr (B == 2) {
+            const uint32_t Pw = w * 130u;
+            group(Pw & 0x780u, w, 0, pos);
+            group(__umulhi(w, 0x00820000u) & 0x780u, w, 2, pos + 2);
+        } else {
+            const uint32_t Pw = w * 0x10204080u;
+            group((Pw >> 21) & 0x780u, w, 0, pos);
+        }
+    };
+    uint4 nx = a + 16 <= b1 ? ldg_v4_na(P.in + a) : make_uint4(0, 0, 0, 0);
+    for (; a + 16 <= b1; a += 16) {
+        const uint4 x = nx;
+        if (a + 32 <= b1) nx = ldg_v4_na(P.in + a + 16);
+        word(x.x, a);
+        word(x.y, a + 4);
+        word(x.z, a + 8);
+        word(x.w, a + 12);
+    }
+    s = (e & 0xFFFFu) >> 11;
+    for (; a < b1; ++a) step1(P.in[a], a);
+}
+
+// The same walk with the rows streamed by TMA (the default for GRID partitions): a
+// thread-per-chunk 16-byte load stream costs 32 L1TEX wavefronts per warp request and the
+// table's shared loads queue behind them (profiles/r02_ncu_find_emit*: 78 % short
+// scoreboard); TMA boxes land in shared memory without that queue.  Warp w of the CTA owns
+// 64 rows (lane l: rows l and l + 32, two chains); 64-row x 64-byte boxes, SWIZZLE_64B, two
+// mbarrier stages; the remainder past the last full row (reading C7) is walked by its lane
+// from global memory.
+constexpr uint32_t kEBox = 64, kERows = 64, kEStages = 2, kEStage = kEBox * kERows, kEThreads = 512;
+
+__host__ __device__ __forceinline__ size_t emit_tma_smem(const DevDfa& d) {
+    return (((size_t)d.Qp * 2048 + (size_t)d.Qp * d.A * 2 + 1023) & ~(size_t)1023) +
+           (kEThreads / 32) * (kEStages * kEStage + 8 * kEStages) + 1024;
+}
+
+template <int B>
+__global__ void __launch_bounds__(kEThreads, 1) find_emit_stride_tma_kernel(const MatchParams P,
+                                                                          const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const DevDfa& d = P.d;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t* tabk32 = reinterpret_cast<uint32_t*>(sm);
+    uint16_t* tab1 = reinterpret_cast<uint16_t*>(sm + (size_t)d.Qp * 2048);
+    const uint32_t sraw = smem_u32(sm);
+    const uint32_t stg = (sraw + (uint32_t)((size_t)d.Qp * 2048 + (size_t)d.Qp * d.A * 2) + 1023u) & ~1023u;
+    const uint32_t stage0 = stg + warp * kEStages * kEStage;
+    const uint32_t mbar0 = stg + nw * kEStages * kEStage + warp * kEStages * 8u;
+    const uint64_t row0 = (uint64_t)blockIdx.x * (nw * kERows) + warp * kERows;
+    const uint32_t nst = (uint32_t)(P.L / kEBox);
+    const bool warp_live = row0 < P.p;
+    if (lane == 0 && warp_live) {
+        for (uint32_t k = 0; k < kEStages; ++k) mbar_init(mbar0 + 8 * k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (uint32_t k = 0; k < kEStages && k < nst; ++k) {
+            mbar_expect_tx(mbar0 + 8 * k, kEStage);
+            tma_load_2d(stage0 + k * kEStage, &tmap, (int32_t)(k * kEBox), (int32_t)row0, mbar0 + 8 * k);
+        }
+    }
+    for (uint32_t i = threadIdx.x; i < d.Qp * 512u; i += blockDim.x) tabk32[i] = __ldg(d.stride + (i >> 5)) | ((i & 31u) << 2);
+    for (uint32_t i = threadIdx.x; i < d.Qp * d.A; i += blockDim.x) tab1[i] = __ldg(d.tab1 + i);
+    __syncthreads();
+    if (!warp_live) return;
+    const unsigned char* tabk = sm;
+    const uint32_t A = d.A, lane4 = lane << 2;
+    const uint64_t ta = row0 + lane, tb = row0 + 32 + lane;
+    const bool la = ta < P.p, lb = tb < P.p;
+    uint32_t ea = ((la ? P.fchunk_q[ta] : 0u) << 11) | lane4, eb = ((lb ? P.fchunk_q[tb] : 0u) << 11) | lane4;
+    unsigned long long oa = la ? P.fchunk_base[ta] : 0ull, ob = lb ? P.fchunk_base[tb] : 0ull;
+    auto step1 = [&](uint32_t& s, unsigned long long& o, uint32_t c, uint64_t k) {
+        const uint32_t e = tab1[s * A + (c < A ? c : A - 1)];
+        s = e & 0x7FFFu;
+        if (e >> 15) {
+            if (o < P.fmax) P.fout[o] = k;
+            ++o;
+        }
+    };
+    // branch-free hot path: a vector's stride groups only OR their hit fields; a vector with
+    // any hit is re-walked symbol by symbol from its entry state (rare for a search
+    // automaton).  A branch per group would expose every lookup's latency.
+    auto group = [&](uint32_t& e, uint32_t& hit, uint32_t g7) {
+        e = *reinterpret_cast<const uint32_t*>(tabk + ((e & 0xFFFFu) | g7));
+        hit |= e;
+    };
+    auto word = [&](uint32_t& e, uint32_t& hit, uint32_t w) {
+        if constexpr (B == 2) {
+            const uint32_t Pw = w * 130u;
+            group(e, hit, Pw & 0x780u);
+            group(e, hit, __umulhi(w, 0x00820000u) & 0x780u);
+        } else {
+            const uint32_t Pw = w * 0x10204080u;
+            group(e, hit, (Pw >> 21) & 0x780u);
+        }
+    };
+    auto rewalk = [&](uint32_t e0, unsigned long long& o, const uint4& v, uint64_t pos) {
+        uint32_t s = (e0 & 0xFFFFu) >> 11;
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+        for (uint32_t q = 0; q < 4; ++q)
+            for (uint32_t j = 0; j < 4; ++j) step1(s, o, (w4[q] >> (8 * j)) & 0xFFu, pos + 4 * q + j);
+    };
+    const uint32_t sw = (lane >> 1) & 3u, offa = lane * kEBox, offb = (lane + 32u) * kEBox;
+    const uint64_t xa = ta * P.L, xb = tb * P.L;
+    uint32_t slot = 0, phase = 0;
+    for (uint32_t st = 0; st < nst; ++st) {
+        mbar_wait(mbar0 + 8 * slot, phase);
+        const uint32_t buf = stage0 + slot * kEStage;
+#pragma unroll
+        for (uint32_t u = 0; u < 4; ++u) {
+            const uint32_t ou = (u ^ sw) << 4;
+            const uint4 va = lds128(buf + offa + ou), vb = lds128(buf + offb + ou);
+            const uint32_t ea0 = ea, eb0 = eb;
+            uint32_t ha = 0, hb = 0;
+            word(ea, ha, va.x);
+            word(eb, hb, vb.x);
+            word(ea, ha, va.y);
+            word(eb, hb, vb.y);
+            word(ea, ha, va.z);
+            word(eb, hb, vb.z);
+            word(ea, ha, va.w);
+            word(eb, hb, vb.w);
+            if (((ha | hb) >> 28) != 0) {
+                if (la && (ha >> 28)) rewalk(ea0, oa, va, xa + st * kEBox + 16 * u);
+                if (lb && (hb >> 28)) rewalk(eb0, ob, vb, xb + st * kEBox + 16 * u);
+            }
+        }
+        __syncwarp();   // every lane consumed the buffer before it is refilled
+        if (lane == 0 && st + kEStages < nst) {
+            mbar_expect_tx(mbar0 + 8 * slot, kEStage);
+            tma_load_2d(buf, &tmap, (int32_t)((st + kEStages) * kEBox), (int32_t)row0, mbar0 + 8 * slot);
+        }
+        if (++slot == kEStages) {
+            slot = 0;
+            phase ^= 1u;
+        }
+    }
+    // the remainder past the last full row belongs to the last chunk (reading C7)
+    if (la && ta == P.p - 1) {
+        uint32_t s = (ea & 0xFFFFu) >> 11;
+        for (uint64_t a = (ta + 1) * P.L; a < P.n; ++a) step1(s, oa, P.in[a], a);
+    }
+    if (lb && tb == P.p - 1) {
+        uint32_t s = (eb & 0xFFFFu) >> 11;
+        for (uint64_t a = (tb + 1) * P.L; a < P.n; ++a) step1(s, ob, P.in[a], a);
+    }
 }
 
 // symbol-major lanes tables (entry = dest * ES | acc << (8 ES - 1)): shared memory when the
@@ -241,7 +431,7 @@ __global__ void __launch_bounds__(kFindThreads) find_emit_lanes_kernel(const Mat
     const uint64_t b0 = find_b(P, t), b1 = find_b(P, t + 1);
     uint32_t e = P.fchunk_q[t] * ES;
     unsigned long long o = P.fchunk_base[t];
-    auto step = [&](uint32_t c, uint64_t k) {
+    auto look = [&](uint32_t c) {
         const uint32_t off = (e & SMASK) | ((c & CMASK) * COL + sbase);
         if constexpr (SMEM) {
             if constexpr (W32) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(off));
@@ -250,10 +440,12 @@ __global__ void __launch_bounds__(kFindThreads) find_emit_lanes_kernel(const Mat
             e = W32 ? __ldg(reinterpret_cast<const uint32_t*>(g + off))
                     : __ldg(reinterpret_cast<const uint16_t*>(g + off));
         }
-        if (e >> ACC) {
-            if (o < P.fmax) P.fout[o] = k;
-            ++o;
-        }
+    };
+    auto step = [&](uint32_t c, uint64_t k) {   // predicated store, no branch
+        look(c);
+        const uint32_t h = e >> ACC;
+        if (h && o < P.fmax) P.fout[o] = k;
+        o += h;
     };
     uint64_t a = b0;
     for (; a < b1 && (((uintptr_t)(P.in + a)) & 15u); ++a) step(P.in[a], a);
@@ -331,7 +523,24 @@ int launch_find(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     prof_after("find_scan_blocks", s);
     find_scan_apply_kernel<<<(unsigned)nb, kScanBlock / 4, 0, s>>>(P);
     prof_after("find_scan", s);
-    if (plan.kernel == kKernelTiny) {
+    CUtensorMap emap;
+    const bool etma = plan.kernel == kKernelTiny && P.d.sym_bits && plan.policy == PAREM_BOUNDARY_GRID &&
+                      !(((uintptr_t)P.in) & 15u) && P.L % kEBox == 0 && P.L >= kEBox && P.p * P.L <= P.n &&
+                      emit_tma_smem(P.d) <= 232448 && encode_rows_map(&emap, P.in, P.L, P.p, kEBox, kERows);
+    if (etma) {
+        const size_t smem = emit_tma_smem(P.d);
+        const void* fn = P.d.sym_bits == 2 ? (const void*)find_emit_stride_tma_kernel<2>
+                                           : (const void*)find_emit_stride_tma_kernel<1>;
+        smem_optin(fn, smem);
+        void* args[] = {const_cast<MatchParams*>(&P), &emap};
+        cudaLaunchKernel(fn, dim3(nblk(p, kEThreads * 2)), dim3(kEThreads), args, smem, s);
+    } else if (plan.kernel == kKernelTiny && P.d.sym_bits) {
+        const size_t smem = (size_t)P.d.Qp * 2048 + (size_t)P.d.Qp * P.d.A * 2;
+        const void* fn = P.d.sym_bits == 2 ? (const void*)find_emit_stride_kernel<2> : (const void*)find_emit_stride_kernel<1>;
+        smem_optin(fn, smem);
+        void* args[] = {const_cast<MatchParams*>(&P)};
+        cudaLaunchKernel(fn, dim3(nblk(p, kFindThreads)), dim3(kFindThreads), args, smem, s);
+    } else if (plan.kernel == kKernelTiny) {
         const size_t smem = (size_t)P.d.Qp * P.d.A * 2;
         find_emit_tiny_kernel<<<nblk(p, kFindThreads), kFindThreads, smem, s>>>(P);
     } else {

@@ -254,6 +254,22 @@ def test_configs_full_size(parem, torch_mod, k):
     assert (got.final_state, got.accepted, got.match_count) == (ref.final_state, ref.accepted, ref.match_count)
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("k,cap", [(1, None), (2, None), (3, 1 << 24)])
+def test_find_positions_full_size(parem, torch_mod, k, cap):
+    """NEXT-4 at full BASELINE size, default launch configuration: the match end offsets of
+    parem_find_async equal the oracle's element by element (every position for cfg1 / cfg2;
+    the first 2^24 of cfg3's ~5e8, whose total count must match too)."""
+    c = synth.config(k)
+    x = c.make_input()
+    want, total = oracle.positions(c.table, c.start, c.accept, x, cap)
+    with parem.Dfa(c.table, c.start, c.accept) as d:
+        r, pos = d.find(torch_mod.from_numpy(x).to("cuda"), max_positions=cap)
+    assert r.status == 0 and r.match_count == total
+    got = pos.cpu().numpy().astype(np.uint64)
+    assert got.size == want.size and np.array_equal(got, want)
+
+
 # ---------------------------------------------------------------- route merging stress
 @pytest.mark.parametrize("Q", [3, 5, 13, 31])
 def test_permutation_dfa_routes_never_merge(parem, torch_mod, Q):
