@@ -639,6 +639,26 @@ def run_config(k: int, args, dist, rank: int, ws_: int, dev, micro: Micro, headl
                          "note": "parem_find_async: the match plus every match end offset (NEXT-4)"}
         del fws, fpos
 
+    # ---- §8(e): ONE input sharded over the ranks (strong scaling of a single input): every
+    # rank holds n / N bytes, computes its segment map, one all-gather, fold on every rank.
+    # Only meaningful under torchrun (N > 1); wall-clock around the synchronous calls.
+    if dist is not None and not args.no_shard:
+        seg_n = n // ws_
+        seg = xd[:seg_n]
+        prev = int(x[seg_n - 1]) if rank > 0 else -1   # this rank's input stands in for T's bytes
+        P.shard_match(dfa, seg, prev, rank * seg_n)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            sr = P.shard_match(dfa, seg, prev, rank * seg_n)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t_sh = reduce_max((time.perf_counter() - t0) / 3, dist, dev)
+        entry["sharded"] = {"value": round(seg_n * ws_ / t_sh / 1e9, 2), "unit": UNIT, "ms_per_step": round(1e3 * t_sh, 3),
+                            "bytes_per_rank": seg_n, "status": sr.status,
+                            "note": "one input of N x bytes_per_rank split over the ranks: parem_segment_map + one "
+                                    "all-gather of the maps + fold (SURVEY §8(e)); host wall clock, max over ranks"}
     if not args.no_cpu_baseline and rank == 0 and ws_ == 1:
         entry["cpu_baseline"] = cpu_baseline(cfg, x)
     if args.verify and rank == 0:
@@ -674,12 +694,14 @@ def main():
     ap.add_argument("--no-find", action="store_true")
     ap.add_argument("--no-enum", action="store_true")
     ap.add_argument("--no-lanes", action="store_true")
+    ap.add_argument("--no-shard", action="store_true")
     ap.add_argument("--quick", action="store_true", help="main measurement only (no e2e/find/enum/lanes/cpu)")
     ap.add_argument("--ref-sample", type=int, default=64 << 20)
     ap.add_argument("--verify", action="store_true", help="bit-exact check against the oracle (full size)")
     args = ap.parse_args()
     if args.quick:
         args.no_e2e = args.no_find = args.no_enum = args.no_lanes = args.no_cpu_baseline = args.no_graph = True
+        args.no_shard = True
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

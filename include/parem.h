@@ -147,6 +147,41 @@ int parem_match_batch_async(const parem_dfa* dfa, const uint8_t* d_input, uint64
                             size_t ws_bytes, const parem_options* opts, parem_result* d_results,
                             void* stream /* cudaStream_t */);
 
+/* ---- one input sharded over G GPUs ----
+ * The paper splits T into parts matched independently and joins their routes (P:67, P:70,
+ * P:114-115).  GPU g holds segment g (bytes [o_g, o_g + n_g) of T) and computes its
+ * SEGMENT MAP over the paper's candidate set for the segment's first position,
+ * R = L(last byte of segment g-1) ({q0} for segment 0): map[r] =
+ * (state after the segment, matches in it) for every r in R.  The G maps (Q entries of
+ * 16 bytes each) are exchanged with one all-gather and folded along q0's path.
+ *
+ * parem_segment_map (synchronous): prev_symbol = the last byte of the previous segment
+ * (-1 for segment 0); h_map: host array of num_states entries (entries outside R have
+ * valid = 0); *status / *bad_offset: PAREM_OK or PAREM_ESYMBOL with the smallest bad
+ * offset LOCAL to the segment.  Routes from R merge (Table II): every candidate
+ * walks a head of X bytes on the device, each distinct state reached is finished with one
+ * ordinary match; a segment on which routes never merge is walked whole from every
+ * candidate (correct, slow).  Allocates its own device scratch. */
+typedef struct parem_segmap_entry {
+    uint64_t match_count;     /* matches inside the segment from this entering state */
+    uint32_t end_state;       /* state after the segment, PAREM_DEAD if the walk died */
+    uint32_t valid;           /* 1: the entering state is a candidate (in R)          */
+} parem_segmap_entry;
+int parem_segment_map(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, int32_t prev_symbol,
+                      const parem_options* opts, parem_segmap_entry* h_map, int32_t* status, uint64_t* bad_offset,
+                      void* stream /* cudaStream_t */);
+
+/* Fold G segment maps (host memory, G x num_states entries, segment-major) along q0's path:
+ * the join of P:70 over segments.  statuses/bad_offsets: per segment (as returned by
+ * parem_segment_map), seg_offsets: o_g (global offset of each segment's first byte).
+ * Writes final state, accept flag, match count and the earliest ESYMBOL (global offset) to
+ * *out (num_chunks = G, routes / route_steps = 0).  Host-only, no device needed.  Returns
+ * PAREM_EINTERNAL if the path enters a state that is not a candidate of the next segment
+ * (cannot happen for maps built from the paper's rule: it is sound, reading C1). */
+int parem_fold_segment_maps(uint32_t num_states, uint32_t start_state, const uint8_t* accept_bitmap,
+                            const parem_segmap_entry* maps, uint32_t G, const int32_t* statuses,
+                            const uint64_t* bad_offsets, const uint64_t* seg_offsets, parem_result* out);
+
 /* Like parem_match_async, but the walk continues from a previous segment's result:
  * the start state is d_carry->final_state (PAREM_DEAD stays dead), counts add to
  * d_carry->match_count and bad offsets are reported as offset_base + local offset

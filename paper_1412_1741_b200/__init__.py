@@ -22,7 +22,7 @@ from ._abi import (BOUNDARY_AUTO, BOUNDARY_GRID, BOUNDARY_SNAP, CANDIDATES_ENUM,
                    KERNEL_TINY, PAREM_DEAD, PAREM_EINVAL, PAREM_ESYMBOL, PAREM_OK)
 
 __all__ = ["Dfa", "MatchResult", "ParemError", "Regex", "compile_regex", "options", "profile", "profile_read", "PAREM_DEAD", "PAREM_OK",
-           "PAREM_ESYMBOL", "PAREM_EINVAL", "lib"]
+           "PAREM_ESYMBOL", "PAREM_EINVAL", "lib", "SEGMAP_DTYPE", "fold_segment_maps", "exchange_and_fold", "shard_match"]
 
 
 def lib():
@@ -132,6 +132,64 @@ def profile_read() -> list[tuple[int, str, float]]:
     return [(int(buf[i].match), buf[i].name.decode(), float(buf[i].ms)) for i in range(n.value)]
 
 
+# parem_segmap_entry (include/parem.h): one per entering state of a segment
+SEGMAP_DTYPE = np.dtype([("match_count", "<u8"), ("end_state", "<u4"), ("valid", "<u4")])
+
+
+def fold_segment_maps(num_states: int, start: int, accept, maps, statuses, bad_offsets, seg_offsets) -> "MatchResult":
+    """parem_fold_segment_maps: fold G segment maps (array (G, num_states) of SEGMAP_DTYPE)
+    along q0's path -- the join of P:70 over the segments of a sharded input.  Host only."""
+    L = lib()
+    m = np.ascontiguousarray(maps, dtype=SEGMAP_DTYPE)
+    G = m.shape[0] if m.ndim == 2 else 0
+    a = np.asarray(accept)
+    bm = np.packbits(a.astype(bool), bitorder="little") if a.dtype == bool else np.ascontiguousarray(a, np.uint8)
+    st = np.ascontiguousarray(statuses, dtype=np.int32)
+    bo = np.ascontiguousarray(bad_offsets, dtype=np.uint64)
+    so = np.ascontiguousarray(seg_offsets, dtype=np.uint64)
+    r = _abi.parem_result()
+    rc = L.parem_fold_segment_maps(num_states, start, bm.ctypes.data, m.ctypes.data, G, st.ctypes.data, bo.ctypes.data,
+                                   so.ctypes.data, C.byref(r))
+    if rc not in (PAREM_OK, PAREM_ESYMBOL):
+        _err(L, rc)
+    return MatchResult.from_struct(r)
+
+
+def exchange_and_fold(segmap, status: int, bad_offset: int, seg_offset: int, num_states: int, start: int,
+                      accept_bitmap, group=None, device=None) -> "MatchResult":
+    """The exchange step of a sharded match: ONE all-gather of every rank's segment map
+    (num_states x 16 bytes) and (status, bad offset, segment offset), then the fold along
+    q0's path on every rank.  Works on any torch.distributed backend (NCCL on GPUs, gloo
+    on CPU)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    dev = device if device is not None else torch.device("cpu")
+    mine = torch.from_numpy(np.ascontiguousarray(segmap, dtype=SEGMAP_DTYPE).view(np.uint8).copy()).to(dev)
+    meta = torch.tensor([status, bad_offset, seg_offset], dtype=torch.int64, device=dev)
+    allm = torch.empty(world * mine.numel(), dtype=torch.uint8, device=dev)
+    allmeta = torch.empty(world * 3, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allm, mine, group=group)
+    dist.all_gather_into_tensor(allmeta, meta, group=group)
+    maps = allm.cpu().numpy().view(SEGMAP_DTYPE).reshape(world, num_states)
+    mt = allmeta.cpu().numpy().reshape(world, 3)
+    return fold_segment_maps(num_states, start, accept_bitmap, maps, mt[:, 0], mt[:, 1].astype(np.uint64),
+                             mt[:, 2].astype(np.uint64))
+
+
+def shard_match(dfa: "Dfa", x_local, prev_symbol: int, seg_offset: int, group=None) -> "MatchResult":
+    """One input sharded over the ranks of a torch.distributed group: this
+    rank's segment map (parem_segment_map over the paper's candidate set for its first
+    position), then exchange_and_fold.  ``prev_symbol`` = last byte of the previous rank's
+    segment (-1 on rank 0), ``seg_offset`` = global offset of this segment's first byte."""
+    import torch.distributed as dist
+
+    m, status, bad = dfa.segment_map(x_local, prev_symbol)
+    dev = x_local.device if dist.get_backend(group) == "nccl" else None
+    return exchange_and_fold(m, status, bad, seg_offset, dfa.Q, dfa.start, dfa.accept_bitmap, group, dev)
+
+
 def _err(L, status: int):
     raise ParemError(status, L.parem_last_error().decode(errors="replace"))
 
@@ -180,6 +238,7 @@ class Dfa:
             _err(self._L, st)
         self._h = h
         self.Q, self.A, self.start = Q, A, int(start)
+        self.accept_bitmap = bm[: (Q + 7) // 8].copy()
 
     # -- lifetime --
     def close(self):
@@ -274,6 +333,21 @@ class Dfa:
         self.match_batch_async(x, ws, res, opts)
         b = res.cpu().numpy().tobytes()
         return [MatchResult.from_bytes(b[56 * i: 56 * (i + 1)]) for i in range(count)]
+
+    def segment_map(self, x, prev_symbol: int, opts=None):
+        """parem_segment_map: this segment's map over the candidate set of its first
+        position (L(prev_symbol); {q0} if prev_symbol < 0).  Returns (map array of
+        SEGMAP_DTYPE with num_states entries, status, local bad offset)."""
+        x = _cuda_u8(x)
+        m = np.zeros(self.Q, dtype=SEGMAP_DTYPE)
+        st = C.c_int32(0)
+        bad = C.c_uint64(0)
+        rc = self._L.parem_segment_map(self._h, C.c_void_p(x.data_ptr()) if x.numel() else None, x.numel(),
+                                       int(prev_symbol), C.byref(opts) if opts is not None else None, m.ctypes.data,
+                                       C.byref(st), C.byref(bad), _stream(None))
+        if rc != PAREM_OK:
+            _err(self._L, rc)
+        return m, int(st.value), int(bad.value)
 
     def find_workspace_bytes(self, n: int, opts=None) -> int:
         ws = self._L.parem_find_workspace_bytes(self._h, n, C.byref(opts) if opts is not None else None)

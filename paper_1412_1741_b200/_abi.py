@@ -62,7 +62,7 @@ EXPORTS = [
     "parem_match_continue_async", "parem_match", "parem_match_host", "parem_dfa_get_info", "parem_plan",
     "parem_last_error", "parem_version", "parem_bench_read_stream", "parem_bench_gather", "parem_profile",
     "parem_profile_read", "parem_regex_compile", "parem_find_async", "parem_find_workspace_bytes",
-    "parem_batch_workspace_bytes", "parem_match_batch_async",
+    "parem_batch_workspace_bytes", "parem_match_batch_async", "parem_segment_map", "parem_fold_segment_maps",
 ]
 
 _LIB = None
@@ -93,6 +93,10 @@ def load(path: str = SO_PATH):
     L.parem_batch_workspace_bytes.argtypes = [vp, u64, u64, O]
     L.parem_match_batch_async.restype = i32
     L.parem_match_batch_async.argtypes = [vp, vp, u64, u64, vp, sz, O, vp, vp]
+    L.parem_segment_map.restype = i32
+    L.parem_segment_map.argtypes = [vp, vp, u64, C.c_int32, O, vp, C.POINTER(C.c_int32), C.POINTER(u64), vp]
+    L.parem_fold_segment_maps.restype = i32
+    L.parem_fold_segment_maps.argtypes = [u32, u32, vp, vp, u32, vp, vp, vp, R]
     L.parem_match.restype = i32
     L.parem_match.argtypes = [vp, vp, u64, O, R, vp]
     L.parem_match_host.restype = i32

@@ -4,6 +4,7 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <string>
@@ -294,6 +295,155 @@ extern "C" int parem_match_batch_async(const parem_dfa* dfa, const uint8_t* d_in
         if (rc != PAREM_OK) return rc;
     }
     return PAREM_OK;
+}
+
+// ---- sharding one input over GPUs: segment maps and their fold ----
+extern "C" int parem_segment_map(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, int32_t prev_symbol,
+                                 const parem_options* opts, parem_segmap_entry* h_map, int32_t* status,
+                                 uint64_t* bad_offset, void* stream_) {
+    set_error("");
+    if (!dfa || !h_map || !status || !bad_offset || (n && !d_input)) { set_error("null argument"); return PAREM_EINVAL; }
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const DevDfa& d = dfa->dev;
+    const uint32_t Q = dfa->Q;
+    for (uint32_t q = 0; q < Q; ++q) h_map[q] = parem_segmap_entry{0, 0, 0};
+    *status = PAREM_OK;
+    *bad_offset = 0;
+    // candidates R: {q0} for the first segment, else L(prev) (all of Q after an invalid byte:
+    // the previous segment reports that ESYMBOL)
+    uint32_t loff = 0, ncand = 1;
+    const bool first = prev_symbol < 0;
+    if (!first) {
+        const uint32_t li = (uint32_t)prev_symbol < dfa->A ? (uint32_t)prev_symbol : dfa->A;
+        cudaError_t e = cudaMemcpy(&loff, d.Loff + li, 4, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemcpy(&ncand, d.Lcnt + li, 4, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) { set_error("segment map: %s", cudaGetErrorString(e)); return PAREM_ECUDA; }
+    }
+    std::vector<uint32_t> cand(ncand);
+    if (first) cand[0] = dfa->start;
+    else if (ncand && cudaMemcpy(cand.data(), d.Llist + loff, 4ull * ncand, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        set_error("segment map: candidate copy failed");
+        return PAREM_ECUDA;
+    }
+    if (ncand == 0) return PAREM_OK;   // R empty (C10): nothing can enter this segment alive
+    if (n == 0) {
+        for (uint32_t r : cand) h_map[r] = parem_segmap_entry{0, r, 1};
+        return PAREM_OK;
+    }
+    // device scratch: candidates, head states, head hits, bad offset, carry + result
+    const size_t c4 = (4ull * ncand + 255) & ~255ull, c8 = (8ull * ncand + 255) & ~255ull;
+    void* blk = nullptr;
+    cudaError_t e = cudaMalloc(&blk, 2 * c4 + c8 + 512);
+    if (e != cudaSuccess) { set_error("cudaMalloc: %s", cudaGetErrorString(e)); return PAREM_ENOMEM; }
+    uint32_t* d_cand = static_cast<uint32_t*>(blk);
+    uint32_t* d_st = reinterpret_cast<uint32_t*>(static_cast<char*>(blk) + c4);
+    unsigned long long* d_hits = reinterpret_cast<unsigned long long*>(static_cast<char*>(blk) + 2 * c4);
+    unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(static_cast<char*>(blk) + 2 * c4 + c8);
+    parem_result* d_res = reinterpret_cast<parem_result*>(static_cast<char*>(blk) + 2 * c4 + c8 + 256);
+    int rc = PAREM_OK;
+    std::vector<uint32_t> st(ncand);
+    std::vector<unsigned long long> hits(ncand);
+    unsigned long long bad_inv = 0;
+    // head length: a multiple of the create-time convergence probe, grown until the heads
+    // end in <= 32 distinct states (or cover the whole segment)
+    const uint64_t conv = dfa->conv_t1 ? dfa->conv_t1 : (dfa->conv_t4 ? 4ull * dfa->conv_t4 : 1024);
+    uint64_t X = std::min<uint64_t>(n, std::max<uint64_t>(4096, 4 * conv));
+    std::vector<uint32_t> zs;
+    e = cudaMemcpyAsync(d_cand, cand.data(), 4ull * ncand, cudaMemcpyHostToDevice, stream);
+    for (;;) {
+        if (e == cudaSuccess) e = cudaMemsetAsync(d_bad, 0, 8, stream);
+        if (e != cudaSuccess) { set_error("segment map: %s", cudaGetErrorString(e)); rc = PAREM_ECUDA; break; }
+        rc = launch_segment_head(d, d_input, X, d_cand, ncand, d_st, d_hits, d_bad, stream);
+        if (rc != PAREM_OK) break;
+        e = cudaMemcpyAsync(st.data(), d_st, 4ull * ncand, cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hits.data(), d_hits, 8ull * ncand, cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&bad_inv, d_bad, 8, cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) { set_error("segment map: %s", cudaGetErrorString(e)); rc = PAREM_ECUDA; break; }
+        zs.assign(st.begin(), st.end());
+        std::sort(zs.begin(), zs.end());
+        zs.erase(std::unique(zs.begin(), zs.end()), zs.end());
+        if (zs.size() <= 32 || X == n) break;
+        X = std::min<uint64_t>(n, 4 * X);
+    }
+    // finish every distinct head state over [X, n) with one ordinary match
+    std::vector<uint32_t> zend(zs.size());
+    std::vector<uint64_t> zcnt(zs.size(), 0);
+    if (rc == PAREM_OK && X < n) {
+        const size_t ws = parem_workspace_bytes(dfa, n - X, opts);
+        void* d_ws = nullptr;
+        if (!ws || cudaMalloc(&d_ws, ws) != cudaSuccess) { set_error("segment map: workspace"); rc = PAREM_ENOMEM; }
+        for (size_t j = 0; rc == PAREM_OK && j < zs.size(); ++j) {
+            parem_result carry;
+            memset(&carry, 0, sizeof(carry));
+            carry.final_state = zs[j] == d.sink && d.has_sink ? PAREM_DEAD : zs[j];
+            parem_result r;
+            e = cudaMemcpyAsync(d_res, &carry, sizeof(carry), cudaMemcpyHostToDevice, stream);
+            if (e == cudaSuccess) e = cudaMemsetAsync(d_ws, 0, 64, stream);
+            if (e != cudaSuccess) { set_error("segment map: %s", cudaGetErrorString(e)); rc = PAREM_ECUDA; break; }
+            rc = match_impl(dfa, d_input + X, n - X, X, d_ws, ws, opts, d_res, d_res, stream);
+            if (rc != PAREM_OK) break;
+            e = cudaMemcpyAsync(&r, d_res, sizeof(r), cudaMemcpyDeviceToHost, stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+            if (e != cudaSuccess) { set_error("segment map: %s", cudaGetErrorString(e)); rc = PAREM_ECUDA; break; }
+            if (r.status == PAREM_ESYMBOL) {
+                *status = PAREM_ESYMBOL;
+                *bad_offset = r.bad_offset;   // offset_base X: local to the segment
+            } else if (r.status != PAREM_OK) {
+                rc = r.status;
+                break;
+            }
+            zend[j] = r.final_state;
+            zcnt[j] = r.match_count;
+        }
+        if (d_ws) cudaFree(d_ws);
+    }
+    cudaFree(blk);
+    if (rc != PAREM_OK) return rc;
+    if (bad_inv) {   // an invalid byte inside the head comes first
+        *status = PAREM_ESYMBOL;
+        *bad_offset = ~bad_inv;
+    }
+    for (uint32_t i = 0; i < ncand; ++i) {
+        const size_t j = std::lower_bound(zs.begin(), zs.end(), st[i]) - zs.begin();
+        uint32_t end = X < n ? zend[j] : st[i];
+        if (X == n && d.has_sink && end == d.sink) end = PAREM_DEAD;
+        h_map[cand[i]] = parem_segmap_entry{hits[i] + (X < n ? zcnt[j] : 0ull), end, 1u};
+    }
+    return PAREM_OK;
+}
+
+extern "C" int parem_fold_segment_maps(uint32_t Q, uint32_t q0, const uint8_t* accept_bitmap,
+                                       const parem_segmap_entry* maps, uint32_t G, const int32_t* statuses,
+                                       const uint64_t* bad_offsets, const uint64_t* seg_offsets, parem_result* out) {
+    if (!out || !accept_bitmap || (G && (!maps || !statuses || !bad_offsets || !seg_offsets)) || q0 >= Q) {
+        set_error("null argument");
+        return PAREM_EINVAL;
+    }
+    parem_result r;
+    memset(&r, 0, sizeof(r));
+    r.num_chunks = G;
+    uint32_t q = q0;
+    uint64_t count = 0;
+    for (uint32_t g = 0; g < G; ++g) {
+        if (statuses[g] == PAREM_ESYMBOL && r.status != PAREM_ESYMBOL) {
+            r.status = PAREM_ESYMBOL;
+            r.bad_offset = seg_offsets[g] + bad_offsets[g];
+        }
+        if (q == PAREM_DEAD) continue;   // a dead walk stays dead (reading C9)
+        const parem_segmap_entry& e = maps[(uint64_t)g * Q + q];
+        if (!e.valid) {
+            set_error("segment %u entered in state %u, not one of its candidates", g, q);
+            return PAREM_EINTERNAL;
+        }
+        count += e.match_count;
+        q = e.end_state;
+    }
+    r.final_state = q;
+    r.accepted = q != PAREM_DEAD && ((accept_bitmap[q >> 3] >> (q & 7)) & 1);
+    r.match_count = count;
+    *out = r;
+    return r.status;
 }
 
 extern "C" int parem_match_continue_async(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n,

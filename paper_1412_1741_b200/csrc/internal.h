@@ -160,6 +160,8 @@ void find_bind(const Plan& plan, MatchParams& P, unsigned char* extra);
 size_t conv_ws_total(uint64_t p);
 size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap, uint32_t warps);
 int launch_trivial(const MatchParams& P, cudaStream_t s);
+int launch_segment_head(const DevDfa& d, const uint8_t* in, uint64_t X, const uint32_t* cand, uint32_t ncand,
+                        uint32_t* st_out, unsigned long long* hits_out, unsigned long long* bad_inv, cudaStream_t s);
 bool encode_rows_map(CUtensorMap* map, const uint8_t* base, uint64_t row_len, uint64_t rows, uint32_t box_w,
                      uint32_t box_rows);
 int tiny_blocks_per_sm(uint32_t K, uint32_t B, bool tma, size_t smem);
