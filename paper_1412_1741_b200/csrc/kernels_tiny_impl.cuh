@@ -29,6 +29,15 @@ struct TinySmem {
     size_t tabk, tab1, lcnt, loff, llist, uni, mend, mhits, wend, whits, mbar, flag, total;
 };
 
+// Row strides of the per-lane dense maps in shared memory.  Lane l writes ITS row (all
+// Qpad entries) while the warp's composition reads one row at the lanes' own states: with
+// a plain Qpad stride the writes of 32 lanes hit the same banks (86.8 % of the store
+// wavefronts conflicted, profiles/r01_ncu_full_cfg2_details.txt).  An odd word stride for
+// the u32 hits (Qpad + 1) and a 5-word stride for the u8 ends make both patterns
+// conflict-free (lane rows land on distinct banks; a read row spreads the lanes' states).
+__host__ __device__ __forceinline__ uint32_t tiny_mend_stride(uint32_t Qpad) { return (Qpad < 4 ? 4u : Qpad) + 4u; }
+__host__ __device__ __forceinline__ uint32_t tiny_mhits_stride(uint32_t Qpad) { return Qpad + 1u; }
+
 // Offsets relative to a 1024-aligned base (the kernel aligns the dynamic smem pointer).
 // `stages` = TMA stages per warp (0: no TMA staging).
 __host__ __device__ __forceinline__ TinySmem tiny_layout(uint32_t Qp, uint32_t Qpad, uint32_t A, uint32_t Lsum_all,
@@ -42,11 +51,12 @@ __host__ __device__ __forceinline__ TinySmem tiny_layout(uint32_t Qp, uint32_t Q
     s.llist = o; o = al16(o + 4 * (size_t)Lsum_all);
     // union: TMA stage buffers during the walk, dense chunk maps afterwards
     s.uni = o = al1k(o);
-    // dense maps of ONE row per lane at a time (the two rows of a lane are composed in turn)
-    const size_t maps = al16((size_t)kT * Qpad) + 4 * (size_t)kT * Qpad;
+    // dense maps of ONE row per lane at a time (the two rows of a lane are composed in turn),
+    // rows padded (tiny_map_strides) so the per-lane row writes are bank-conflict free
+    const size_t maps = al16((size_t)kT * tiny_mend_stride(Qpad)) + 4 * (size_t)kT * tiny_mhits_stride(Qpad);
     const size_t stg = (size_t)kWarps * stages * kStageBytes;
     s.mend = s.uni;
-    s.mhits = s.uni + al16((size_t)kT * Qpad);
+    s.mhits = s.uni + al16((size_t)kT * tiny_mend_stride(Qpad));
     o = al16(s.uni + (maps > stg ? maps : stg));
     s.wend = o;  o = al16(o + 4 * (size_t)kWarps * Qpad);
     s.whits = o; o = al16(o + 8 * (size_t)kWarps * Qpad);
@@ -226,6 +236,7 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t S = TMA ? P.stages : 0u;
     const TinySmem L = tiny_layout(Qp, Qpad, A, d.Lsum_all, B, S);
+    const uint32_t MS = tiny_mend_stride(Qpad), HS = tiny_mhits_stride(Qpad);
     uint32_t* tabk32 = reinterpret_cast<uint32_t*>(sm + L.tabk);
     const unsigned char* tabk = sm + L.tabk;
     uint16_t* tab1 = reinterpret_cast<uint16_t*>(sm + L.tab1);
@@ -400,8 +411,8 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
     // ---- per-chunk dense maps (identity for non-candidates), extra passes, validation ----
     auto finish = [&](const TinyChunk& c, Routes<K, B>& r, bool act, uint32_t lr) {
         for (uint32_t q = 0; q < Qpad; ++q) {
-            mend[lr * Qpad + q] = (uint8_t)q;
-            mhits[lr * Qpad + q] = 0;
+            mend[lr * MS + q] = (uint8_t)q;
+            mhits[lr * HS + q] = 0;
         }
         if (!c.live) return;
         uint32_t badacc = act ? r.bad : 0u;
@@ -409,8 +420,8 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
         for (int j = 0; j < K; ++j)
             if ((uint32_t)j < c.cnt) {
                 const uint32_t s = (c.t == 0 || (P.cpi && c.t % P.cpi == 0)) ? c.q0 : tiny_cand(c, Llist, j);
-                mend[lr * Qpad + s] = (uint8_t)r.state(j);
-                mhits[lr * Qpad + s] = r.h[j];
+                mend[lr * MS + s] = (uint8_t)r.state(j);
+                mhits[lr * HS + s] = r.h[j];
             }
         // extra passes for chunks with more than K candidates (SNAP window miss, Enum)
         for (uint32_t base = K; base < c.cnt; base += K) {
@@ -428,14 +439,14 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
             for (int j = 0; j < K; ++j)
                 if (base + (uint32_t)j < c.cnt) {
                     const uint32_t s = tiny_cand(c, Llist, base + j);
-                    mend[lr * Qpad + s] = (uint8_t)x.state(j);
-                    mhits[lr * Qpad + s] = x.h[j];
+                    mend[lr * MS + s] = (uint8_t)x.state(j);
+                    mhits[lr * HS + s] = x.h[j];
                 }
         }
         if (P.fmend) {   // parem_find_async: keep this chunk's dense map for the position pass
             for (uint32_t q = 0; q < Qpad; ++q) {
-                P.fmend[c.t * Qpad + q] = mend[lr * Qpad + q];
-                P.fmhits[c.t * Qpad + q] = mhits[lr * Qpad + q];
+                P.fmend[c.t * Qpad + q] = mend[lr * MS + q];
+                P.fmhits[c.t * Qpad + q] = mhits[lr * HS + q];
             }
         }
         if (c.cnt == 0 && first_bad(P.in, c.b0, c.b1, A) < c.b1) badacc = 1;   // R_i empty: still validate
@@ -454,9 +465,9 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
     auto compose32 = [&]() {
         __syncwarp();
         for (uint32_t i = 0; i < 32; ++i) {
-            const uint32_t row = (warp * 32 + i) * Qpad + wce;
-            const uint32_t ne = mend[row];
-            wch += mhits[row];
+            const uint32_t r = warp * 32 + i;
+            const uint32_t ne = mend[r * MS + wce];
+            wch += mhits[r * HS + wce];
             wce = ne;
         }
         __syncwarp();
