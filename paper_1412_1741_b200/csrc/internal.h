@@ -112,6 +112,7 @@ struct Plan {
     uint32_t tma;            // tiny: TMA stages per warp (0 = rows read with 16-B loads)
     uint32_t dmax;           // conv: set-walk hand-over threshold (1, 2 or 4 survivors)
     uint32_t conv_tma;       // conv: TMA-staged follow walk (rows of L bytes)
+    uint32_t conv_rep;       // conv: follow table replicated in R = 8 / 16 copies (0: plain)
     uint32_t set_own;        // conv: phase-A dedup by owner tags (Qpad <= 1024)
     uint32_t conv_cpt;       // conv: chunks per follow thread (1 or 2)
     uint32_t conv_fthreads;  // conv: follow block size
@@ -158,6 +159,8 @@ int launch_find(const Plan& plan, const MatchParams& P, cudaStream_t s);
 size_t find_extra_bytes(const Plan& plan, const DevDfa& d);
 void find_bind(const Plan& plan, MatchParams& P, unsigned char* extra);
 size_t conv_ws_total(uint64_t p);
+size_t conv_rep_smem(const DevDfa& d, uint32_t R);        // 0 if the layout does not apply
+size_t conv_follow_tma_smem(size_t table_bytes);
 size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap, uint32_t warps);
 int launch_trivial(const MatchParams& P, cudaStream_t s);
 int launch_segment_head(const DevDfa& d, const uint8_t* in, uint64_t X, const uint32_t* cand, uint32_t ncand,

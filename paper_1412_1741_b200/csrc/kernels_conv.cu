@@ -135,7 +135,7 @@ __host__ __device__ __forceinline__ size_t tab_bytes(const DevDfa& d) {
 template <bool SMEM, bool W32>
 struct Tab {
     static constexpr uint32_t ES = W32 ? 4 : 2, ACC = W32 ? 31 : 15;
-    static constexpr bool kSmem = SMEM, kW32 = W32;
+    static constexpr bool kSmem = SMEM, kW32 = W32, kRep = false;
     const unsigned char* g;
     uint32_t cbase, COL, SMASK, CMASK;
 
@@ -185,6 +185,93 @@ __device__ __forceinline__ uint32_t stage_table(const DevDfa& d, unsigned char* 
 
 __host__ __device__ __forceinline__ size_t smem_tab_bytes(const DevDfa& d, bool smem) {
     return smem ? al16(tab_bytes(d) + (size_t)d.Qpad * (d.lanes_u32 ? 4 : 2)) : 0;
+}
+
+// Replicated-fragment table for the follow walk (shared memory, R = 8, 16 or 32 copies of
+// a u16 table): 32 lanes looking up 32 random states of a plain table hit ~3.5 wavefronts
+// per LDS (profiles/r01_ncu_full_cfg3_follow*).  Copy k = lane mod R lives in the banks
+// k + R j (j < 32 / R), so only the 32 / R lanes sharing a copy can conflict, and every
+// entry stores the NEXT state's address fragment within its copy (+ accept bit 15):
+// next = (e & FMASK) | col(c), one LOP3 per lookup as with the plain table.
+//   frag(s, k) = (s >> 1 >> lg) << 7 | ((s >> 1) & (32/R - 1)) * R * 4 | k << 2 | (s & 1) << 1,
+//   lg = log2(32 / R); a column (one symbol) is Qpad * 2 R bytes.
+template <int R>
+__host__ __device__ __forceinline__ uint32_t rep_frag(uint32_t s, uint32_t k) {
+    constexpr uint32_t G = 32 / R, LG = R == 32 ? 0 : R == 16 ? 1 : 2;
+    const uint32_t w = s >> 1;
+    return ((w >> LG) << 7) | ((w & (G - 1u)) * (R * 4u)) | (k << 2) | ((s & 1u) << 1);
+}
+__host__ __device__ __forceinline__ uint32_t rep_col_bytes(uint32_t Qpad, uint32_t R) { return Qpad * 2u * R; }
+
+template <int R>
+struct TabR {
+    static constexpr uint32_t ES = 2;
+    static constexpr bool kSmem = true, kW32 = false, kRep = true;
+    static constexpr int kR = R;
+    uint32_t tbase, COL, FMASK, AM1, k;
+
+    // stage the copies into shared memory at tbase (a multiple of COL) inside [sm, sm + bytes)
+    __device__ __forceinline__ void init(const DevDfa& d, unsigned char* sm) {
+        COL = rep_col_bytes(d.Qpad, R);
+        FMASK = COL - 1u;
+        AM1 = d.A - 1u;
+        k = threadIdx.x & (uint32_t)(R - 1);
+        const uint32_t sraw = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+        tbase = (sraw + COL - 1) / COL * COL;
+        unsigned char* base = sm + (tbase - sraw);
+        const uint32_t total = d.A * d.Qpad;   // one thread per (c, s) entry writes its R copies
+        for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
+            const uint32_t s = i & (d.Qpad - 1u), c = i >> d.log2Qpad;
+            uint32_t dest, acc;
+            if (d.lanes_u32) {
+                const uint32_t e = __ldg(reinterpret_cast<const uint32_t*>(d.lanes_tab) + (size_t)c * d.Qpad + s);
+                dest = (e & ((d.Qpad - 1u) * 4u)) >> 2;
+                acc = e >> 31;
+            } else {
+                const uint32_t e = __ldg(reinterpret_cast<const uint16_t*>(d.lanes_tab) + (size_t)c * d.Qpad + s);
+                dest = (e & ((d.Qpad - 1u) * 2u)) >> 1;
+                acc = e >> 15;
+            }
+            unsigned char* colp = base + (size_t)c * COL;
+#pragma unroll 4
+            for (uint32_t kk = 0; kk < (uint32_t)R; ++kk)
+                *reinterpret_cast<uint16_t*>(colp + rep_frag<R>(s, kk)) = (uint16_t)(rep_frag<R>(dest, kk) | (acc << 15));
+        }
+    }
+    // bytes >= A use column A - 1 (the chunk reports ESYMBOL anyway, reading C11)
+    __device__ __forceinline__ uint32_t col(uint32_t c) const { return min(c, AM1) * COL + tbase; }
+    __device__ __forceinline__ uint32_t colm(uint32_t c) const { return min(c, AM1) * COL + tbase; }
+    __device__ __forceinline__ uint32_t next(uint32_t e, uint32_t colc) const {
+        uint32_t v;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"((e & FMASK) | colc));
+        return v;
+    }
+    __device__ __forceinline__ uint32_t state(uint32_t e) const {
+        constexpr uint32_t G = 32 / R, LG = R == 32 ? 0 : R == 16 ? 1 : 2;
+        const uint32_t f = e & FMASK;
+        const uint32_t w = ((f >> 7) << LG) | ((f >> 2) / R & (G - 1u));
+        return (w << 1) | ((f >> 1) & 1u);
+    }
+    __device__ __forceinline__ uint32_t hit(uint32_t e) const { return e >> 15; }
+    __device__ __forceinline__ uint32_t start(uint32_t s) const { return rep_frag<R>(s, k); }
+    __device__ __forceinline__ uint32_t word_mask() const { return 0xFFFFFFFFu; }
+};
+
+__host__ __device__ __forceinline__ size_t rep_smem_bytes(const DevDfa& d, uint32_t R) {
+    const size_t col = rep_col_bytes(d.Qpad, R);
+    return col > (1u << 15) ? 0 : (size_t)d.A * col + col;   // + alignment slack
+}
+
+// staging and footprint of any follow table type
+template <class TT>
+__device__ __forceinline__ void tab_setup(TT& T, const DevDfa& d, unsigned char* sm) {
+    if constexpr (TT::kRep) T.init(d, sm);
+    else T.init(d, stage_table<TT::kSmem, TT::kW32>(d, sm));
+}
+template <class TT>
+__host__ __device__ __forceinline__ size_t tab_smem(const DevDfa& d) {
+    if constexpr (TT::kRep) return rep_smem_bytes(d, TT::kR);
+    else return smem_tab_bytes(d, TT::kSmem);
 }
 
 __device__ __forceinline__ uint64_t conv_b(const MatchParams& P, uint64_t i) {
@@ -562,7 +649,7 @@ __global__ void __launch_bounds__(1024) conv_follow_kernel(const MatchParams P) 
     extern __shared__ __align__(16) unsigned char sm[];
     const DevDfa& d = P.d;
     TT T;
-    T.init(d, stage_table<TT::kSmem, TT::kW32>(d, sm));
+    tab_setup(T, d, sm);
     __syncthreads();
     const ConvWs W = conv_ws(P);
     const uint8_t* in = P.in;
@@ -661,8 +748,8 @@ __global__ void __launch_bounds__(kFThreads) conv_follow_tma_kernel(const MatchP
     const DevDfa& d = P.d;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     TT T;
-    T.init(d, stage_table<TT::kSmem, TT::kW32>(d, sm));
-    const size_t tb = smem_tab_bytes(d, TT::kSmem);
+    tab_setup(T, d, sm);
+    const size_t tb = tab_smem<TT>(d);
     const uint32_t sraw = smem_u32(sm);
     const uint32_t stg = (sraw + (uint32_t)tb + 1023u) & ~1023u;   // 1024-aligned staging (swizzle atoms)
     const uint32_t stage0 = stg + warp * kFStages * kFStageBytes;
@@ -1209,7 +1296,7 @@ bool launch_follow_tma(const MatchParams& P, size_t tb, cudaStream_t s, cudaErro
     memset(&map, 0, sizeof(map));
     if (!encode_rows_map(&map, P.in, P.L, P.p - 1, kFBox, 32)) return false;
     const void* fn = reinterpret_cast<const void*>(&conv_follow_tma_kernel<TT>);
-    cudaError_t e = smem_optin(fn, follow_tma_smem(tb));
+    cudaError_t e = smem_optin(fn, follow_tma_smem(tb));   // tb = the table type's footprint
     if (e == cudaSuccess) {
         void* args[] = {const_cast<MatchParams*>(&P), &map};
         const unsigned g = (unsigned)((P.p + kFThreads - 1) / kFThreads);
@@ -1250,7 +1337,13 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
         e = cudaLaunchKernel(setfn, dim3(g1), dim3(sw * 32), args, s1, s);
     }
     prof_after("conv_set", s);
-    e = launch_follow_cpt<Tab<SMEM, W32>>(plan, P, tb, s);
+    if constexpr (SMEM) {
+        if (plan.conv_rep == 8) e = launch_follow_cpt<TabR<8>>(plan, P, rep_smem_bytes(d, 8), s);
+        else if (plan.conv_rep == 16) e = launch_follow_cpt<TabR<16>>(plan, P, rep_smem_bytes(d, 16), s);
+        else e = launch_follow_cpt<Tab<SMEM, W32>>(plan, P, tb, s);
+    } else {
+        e = launch_follow_cpt<Tab<SMEM, W32>>(plan, P, tb, s);
+    }
     prof_after("conv_follow", s);
     if (e != cudaSuccess) {
         set_error("conv_follow: %s", cudaGetErrorString(e));
@@ -1294,6 +1387,9 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
 }  // namespace
 
 size_t conv_ws_total(uint64_t p) { return conv_ws_bytes(p); }
+
+size_t conv_rep_smem(const DevDfa& d, uint32_t R) { return rep_smem_bytes(d, R); }
+size_t conv_follow_tma_smem(size_t table_bytes) { return follow_tma_smem(table_bytes); }
 
 size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap, uint32_t warps) {
     return smem_tab_bytes(d, smem_tab) + warps * set_warp_bytes(cap, d.Qpad);

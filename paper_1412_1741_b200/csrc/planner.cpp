@@ -172,6 +172,13 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         plan->conv_tma = 0;
         plan->set_own = 1;
         if (const char* e = getenv("PAREM_CONV_TMA")) plan->conv_tma = (uint32_t)atoi(e);   // experiments
+        plan->conv_rep = 0;
+        if (const char* e = getenv("PAREM_CONV_REP")) plan->conv_rep = (uint32_t)atoi(e);
+        if (plan->conv_rep) {
+            const size_t rb = conv_smem_tab ? conv_rep_smem(d, plan->conv_rep) : 0;
+            const size_t need = plan->conv_tma ? conv_follow_tma_smem(rb) : rb;
+            if (!rb || (plan->conv_rep != 8 && plan->conv_rep != 16) || need > 232448 - 1024) plan->conv_rep = 0;
+        }
         if (const char* e = getenv("PAREM_SET_OWN")) plan->set_own = (uint32_t)atoi(e);
         plan->conv_fthreads = 512;
         plan->conv_cpt = 1;
