@@ -319,15 +319,19 @@ extern "C" int parem_segment_map(const parem_dfa* dfa, const uint8_t* d_input, u
         if (e == cudaSuccess) e = cudaMemcpy(&ncand, d.Lcnt + li, 4, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) { set_error("segment map: %s", cudaGetErrorString(e)); return PAREM_ECUDA; }
     }
+    // R empty (C10): nothing enters this segment alive -- the map stays invalid, but every
+    // byte is still validated (C11): one placeholder walker covers the whole segment
+    const bool empty = ncand == 0;
+    if (empty) ncand = 1;
     std::vector<uint32_t> cand(ncand);
-    if (first) cand[0] = dfa->start;
+    if (first || empty) cand[0] = first ? dfa->start : 0u;
     else if (ncand && cudaMemcpy(cand.data(), d.Llist + loff, 4ull * ncand, cudaMemcpyDeviceToHost) != cudaSuccess) {
         set_error("segment map: candidate copy failed");
         return PAREM_ECUDA;
     }
-    if (ncand == 0) return PAREM_OK;   // R empty (C10): nothing can enter this segment alive
     if (n == 0) {
-        for (uint32_t r : cand) h_map[r] = parem_segmap_entry{0, r, 1};
+        if (!empty)
+            for (uint32_t r : cand) h_map[r] = parem_segmap_entry{0, r, 1};
         return PAREM_OK;
     }
     // device scratch: candidates, head states, head hits, bad offset, carry + result
@@ -347,7 +351,7 @@ extern "C" int parem_segment_map(const parem_dfa* dfa, const uint8_t* d_input, u
     // head length: a multiple of the create-time convergence probe, grown until the heads
     // end in <= 32 distinct states (or cover the whole segment)
     const uint64_t conv = dfa->conv_t1 ? dfa->conv_t1 : (dfa->conv_t4 ? 4ull * dfa->conv_t4 : 1024);
-    uint64_t X = std::min<uint64_t>(n, std::max<uint64_t>(4096, 4 * conv));
+    uint64_t X = empty ? n : std::min<uint64_t>(n, std::max<uint64_t>(4096, 4 * conv));
     std::vector<uint32_t> zs;
     e = cudaMemcpyAsync(d_cand, cand.data(), 4ull * ncand, cudaMemcpyHostToDevice, stream);
     for (;;) {
@@ -404,7 +408,7 @@ extern "C" int parem_segment_map(const parem_dfa* dfa, const uint8_t* d_input, u
         *status = PAREM_ESYMBOL;
         *bad_offset = ~bad_inv;
     }
-    for (uint32_t i = 0; i < ncand; ++i) {
+    for (uint32_t i = 0; i < ncand && !empty; ++i) {
         const size_t j = std::lower_bound(zs.begin(), zs.end(), st[i]) - zs.begin();
         uint32_t end = X < n ? zend[j] : st[i];
         if (X == n && d.has_sink && end == d.sink) end = PAREM_DEAD;

@@ -96,3 +96,15 @@ def test_sharded_esymbol_and_empty(parem, torch_mod):
     expect(parem, torch_mod, c.table, c.start, c.accept, x, [0, 100_000, 200_000, x.size])
     y = c.make_input()
     expect(parem, torch_mod, c.table, c.start, c.accept, y, [0, 150_000, 150_000, y.size])   # empty middle
+
+
+def test_sharded_empty_candidate_set_still_validates(parem, torch_mod):
+    """R = L(previous byte) can be empty (C10: only the sink arrives); the segment's bytes
+    are still validated (C11) -- found by tools/stress.py (seed 537)."""
+    D = 0xFFFF
+    t = np.array([[1, D, 0], [D, D, D]], dtype=np.uint16)   # L(symbol 1) = {} : every entry DEAD
+    acc = np.array([False, True])
+    x = np.array([0, 1, 2, 9, 0, 2], dtype=np.uint8)         # invalid 9 at offset 3
+    expect(parem, torch_mod, t, 0, acc, x, [0, 2, x.size])
+    y = np.array([0, 1, 2, 0, 0, 2], dtype=np.uint8)         # valid: the walk died at offset 1
+    expect(parem, torch_mod, t, 0, acc, y, [0, 2, 4, y.size])

@@ -26,6 +26,9 @@ for seed in range(int(sys.argv[1]) if len(sys.argv) > 1 else 300):
     opts = P.options(chunk_len=int(rng.choice([0, 0, 1, 7, 64, 500, 4096])),
                      boundary=str(rng.choice(["auto", "grid", "snap"])),
                      candidates=str(rng.choice(["parem", "parem", "enum"])))
+    # the converging path's opt-in variants (read by the planner on every call)
+    os.environ["PAREM_CONV_TMA"] = str(int(rng.random() < 0.3))
+    os.environ["PAREM_CONV_REP"] = str(int(rng.choice([0, 0, 8, 16])))
     ref = oracle.walk(t, q0, acc, x)
     buf = torch.empty(n + 32, dtype=torch.uint8, device="cuda")
     off = int(rng.integers(0, 16))
@@ -36,12 +39,28 @@ for seed in range(int(sys.argv[1]) if len(sys.argv) > 1 else 300):
         with P.Dfa(t, q0, acc) as d:
             r = d.match(xd, opts)
             rf, pos = d.find(xd, max_positions=100, opts=opts)
+            # one input sharded into 1..3 segments: segment maps + fold
+            G = int(rng.integers(1, 4))
+            cuts = sorted([0, n] + [int(v) for v in rng.integers(0, n + 1, G - 1)])
+            maps, sts, bads = [], [], []
+            for g in range(G):
+                seg = xd[cuts[g]:cuts[g + 1]]
+                m, st_, b_ = d.segment_map(seg, int(x[cuts[g] - 1]) if cuts[g] > 0 else -1)
+                maps.append(m); sts.append(st_); bads.append(b_)
+            rs = P.fold_segment_maps(Q, q0, d.accept_bitmap, np.stack(maps), sts, bads, cuts[:-1])
+            # the same input twice more as a batch of independent inputs
+            rb = d.match_batch(torch.stack([xd, xd, xd]) if n else xd.reshape(0, 0)) if n else []
         if ref.status == oracle.ESYMBOL:
             ok = r.status == P.PAREM_ESYMBOL and r.bad_offset == ref.bad_offset
+            ok = ok and rs.status == P.PAREM_ESYMBOL and rs.bad_offset == ref.bad_offset
+            ok = ok and all(b.status == P.PAREM_ESYMBOL and b.bad_offset == ref.bad_offset for b in rb)
         else:
             pr, cnt = oracle.positions(t, q0, acc, x, cap=100)
-            ok = (r.status == 0 and (r.final_state, r.accepted, r.match_count) == (ref.final_state, ref.accepted, ref.match_count)
+            want = (ref.final_state, ref.accepted, ref.match_count)
+            ok = (r.status == 0 and (r.final_state, r.accepted, r.match_count) == want
                   and rf.match_count == cnt and pos.cpu().numpy().astype(np.uint64).tolist() == pr.tolist())
+            ok = ok and rs.status == 0 and (rs.final_state, rs.accepted, rs.match_count) == want
+            ok = ok and all(b.status == 0 and (b.final_state, b.accepted, b.match_count) == want for b in rb)
     except Exception as e:
         ok = False
         print("EXC", e)
