@@ -309,7 +309,9 @@ int parem_profile_read(parem_kernel_time* out, int max, int* count);
  *   gather:      every thread performs `steps` dependent random lookups into a table of
  *                table_bytes (uint16 entries) held in shared memory (where=0) or global /
  *                L2 (where=1; indices scattered over the whole table) or in shared memory,
- *                lane-private (where=2); lookups_out = total lookups per launch.  d_sink[0..1]:
+ *                lane-private (where=2); every chain mixes its own pseudo-random stream into
+ *                the next index (chains never coalesce, as routes under different inputs do
+ *                not); lookups_out = total lookups per launch.  d_sink[0..1]:
  *                the kernels write d_sink[0] only if their result equals d_sink[1] (pass
  *                0xFFFFFFFF there), which keeps the loads alive. */
 float parem_bench_read_stream(const uint8_t* d_input, uint64_t n, uint32_t* d_sink, int reps, void* stream);

@@ -611,9 +611,12 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint16_t* __restrict_
     if (WHERE == 2)
         for (uint32_t i = tid; i < entries * 32u; i += blockDim.x) t32[i] = tab[i >> 5];
     __syncthreads();
-    uint32_t x[8];
+    uint32_t x[8], rng[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = (blockIdx.x * 977u + tid * 131u + 37u * k) & mask;
+    for (int k = 0; k < 8; ++k) {
+        x[k] = (blockIdx.x * 977u + tid * 131u + 37u * k) & mask;
+        rng[k] = (blockIdx.x * blockDim.x + tid) * 747796405u + 2891336453u * (uint32_t)(k + 1);
+    }
     for (uint32_t s = 0; s < steps; ++s) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -621,8 +624,14 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint16_t* __restrict_
             if (WHERE == 0) v = t32[x[k]];
             else if (WHERE == 1) v = __ldg(tab + x[k]);
             else v = t32[x[k] * 32u + lane];
-            // scatter over the WHOLE table (v alone would only reach the first 64 Ki entries)
-            x[k] = (v * 0x9E3779B1u + s) & mask;
+            // Next index = loaded value (the "state") + this chain's OWN pseudo-random stream
+            // (the "symbol"), scattered over the whole table.  Round 2's first version added
+            // the step number instead: every chain then applied the SAME map per step, so
+            // chains that met stayed together (the route merging of the paper, in
+            // the benchmark itself), lanes shared addresses and the rate was overstated ~2x
+            // (profiles/r02_follow_probe.txt).
+            rng[k] = rng[k] * 1664525u + 1013904223u;
+            x[k] = ((v + (rng[k] >> 8)) * 0x9E3779B1u >> 7) & mask;
         }
     }
     uint32_t acc = 0;
