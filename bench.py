@@ -441,6 +441,17 @@ def run_config(k: int, args, dist, rank: int, ws_: int, dev, micro: Micro, headl
                   "traffic": latest_traffic(cfg.index, dominant)})
     if bound["traffic"]:
         bound["traffic"]["vs_algorithmic"] = round(bound["traffic"]["dram_bytes_per_launch"] / n, 3)
+    if kern == 3 and r.lookups and G:
+        # What the converging path executed (parem_result.lookups_k: the set walk's deduplicated
+        # sets, the follow's live routes, the join's head walks) against the same gather peak:
+        # the fraction of the level's lookup rate the kernels sustain over the whole step.  The
+        # gap between this and `frac` is the method's speculation work (lookups per byte > 1).
+        lrate = r.lookups / (ms_per_step * 1e-3)
+        bound["executed_lookups"] = {
+            "lookups_per_launch": r.lookups, "per_input_byte": round(r.lookups / n, 4),
+            "rate_per_s": float(f"{lrate:.4g}"), "peak_per_s": float(f"{G:.4g}"),
+            "frac_of_gather_peak": round(lrate / G, 4),
+            "note": "lookups at distinct states counted by the kernels; SURVEY 8(d) def. 4: achieved lookups/s / G_level"}
 
     entry = {
         "workload": f"cfg{cfg.index}: {cfg.name}", "n_bytes": n, "states": cfg.Q, "alphabet": cfg.A,
@@ -504,7 +515,7 @@ def run_config(k: int, args, dist, rank: int, ws_: int, dev, micro: Micro, headl
                                 "cold_gbs": round(n / (statistics.median(cold) * 1e-3) / 1e9, 2),
                                 "note": "one match per launch sequence, CUDA events; cold = after writing 2x L2"}
         if not args.no_graph:
-            K = max(8, (2 * L2_BYTES + 4 * n) // n)
+            K = max(8, (4 * L2_BYTES + 4 * n) // n)   # K n >= 4x L2 (SURVEY §8(d) note 1): HBM-honest
             bufs = torch.empty((K, n), dtype=torch.uint8, device=dev)
             for i in range(K):
                 bufs[i].copy_(torch.from_numpy(rank_input(cfg, rank * K + i)))

@@ -62,7 +62,9 @@ extern "C" {
 
 /* Result of one match (56 bytes).  routes = sum_i |R_i| ("calculations"; with
  * |R_0| = 1), route_steps = sum_i |R_i| * len_i (candidate-steps, the lookup roofline's
- * work), num_chunks = p. */
+ * work), num_chunks = p.  lookups_k reports what the converging path actually executed after
+ * merging routes that met (set walk: the deduplicated set per step; follow and head walks: the
+ * live routes), for the lookup roofline of DESIGN.md section 7. */
 typedef struct parem_result {
     uint64_t match_count;
     uint32_t final_state;
@@ -72,7 +74,8 @@ typedef struct parem_result {
     uint64_t routes;
     uint64_t route_steps;
     int32_t status;
-    uint32_t reserved;
+    uint32_t lookups_k;   /* diagnostic: table lookups issued at distinct states by the converging
+                             path's kernels, in units of 1024 (0 on the other paths) */
 } parem_result;
 
 /* Options (NULL = defaults: planner-chosen chunk length, AUTO boundaries, PaREM candidates).

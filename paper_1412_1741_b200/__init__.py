@@ -44,11 +44,12 @@ class MatchResult(NamedTuple):
     num_chunks: int
     routes: int               # sum |R_i|   ("calculations")
     route_steps: int          # sum |R_i| * len_i
+    lookups: int = 0          # converging path: lookups issued at distinct states (multiple of 1024)
 
     @staticmethod
     def from_struct(r: _abi.parem_result) -> "MatchResult":
         return MatchResult(r.final_state, bool(r.accepted), r.match_count, r.status, r.bad_offset, r.num_chunks,
-                           r.routes, r.route_steps)
+                           r.routes, r.route_steps, int(r.lookups_k) << 10)
 
     @staticmethod
     def from_bytes(b: bytes) -> "MatchResult":

@@ -17,7 +17,7 @@ KERNEL_AUTO, KERNEL_TINY, KERNEL_LANES, KERNEL_CONV = 0, 1, 2, 3
 class parem_result(C.Structure):
     _fields_ = [("match_count", C.c_uint64), ("final_state", C.c_uint32), ("accepted", C.c_uint32),
                 ("bad_offset", C.c_uint64), ("num_chunks", C.c_uint64), ("routes", C.c_uint64),
-                ("route_steps", C.c_uint64), ("status", C.c_int32), ("reserved", C.c_uint32)]
+                ("route_steps", C.c_uint64), ("status", C.c_int32), ("lookups_k", C.c_uint32)]
 
 
 class parem_options(C.Structure):

@@ -630,8 +630,15 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint16_t* __restrict_
             // chains that met stayed together (the route merging of the paper, in
             // the benchmark itself), lanes shared addresses and the rate was overstated ~2x
             // (profiles/r02_follow_probe.txt).
-            rng[k] = rng[k] * 1664525u + 1013904223u;
-            x[k] = ((v + (rng[k] >> 8)) * 0x9E3779B1u >> 7) & mask;
+            // Lane-private tables (WHERE == 2) cannot share addresses between chains, so they
+            // keep the cheap index update: the added arithmetic would make that probe
+            // issue-bound instead of shared-memory-bound.
+            if (WHERE == 2) {
+                x[k] = (v * 0x9E3779B1u + s) & mask;
+            } else {
+                rng[k] = rng[k] * 1664525u + 1013904223u;
+                x[k] = ((v + (rng[k] >> 8)) * 0x9E3779B1u >> 7) & mask;
+            }
         }
     }
     uint32_t acc = 0;

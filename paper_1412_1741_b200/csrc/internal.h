@@ -54,7 +54,9 @@ struct WsHeader {              // first 64 bytes of every workspace (memset to 0
     unsigned long long hits;     // conv path: total hits along the true path
     unsigned int final_q;        // conv path: state after the last chunk
     unsigned int pad;
-    unsigned long long pad2[2];
+    unsigned long long lookups;  // conv path: table lookups issued at distinct states (set walk:
+                                 // the deduplicated set per step; follow / head walks: live routes)
+    unsigned long long pad2;
 };
 static_assert(sizeof(WsHeader) == 64, "header");
 

@@ -119,6 +119,7 @@ __device__ __forceinline__ void reset_header(const MatchParams& P) {
     h->routes = 0;
     h->steps = 0;
     h->hits = 0;
+    h->lookups = 0;
     h->final_q = 0;
     __threadfence();
 }
@@ -147,7 +148,7 @@ __device__ __forceinline__ void write_result(const MatchParams& P, uint32_t q, u
     r.num_chunks = base_chunks + P.p;
     r.routes = base_routes + h->routes;
     r.route_steps = base_steps + h->steps;
-    r.reserved = 0;
+    r.lookups_k = (uint32_t)min((h->lookups + 1023ull) >> 10, 0xFFFFFFFFull);
     const unsigned long long binv = h->bad_inv;
     if (cst == PAREM_ESYMBOL) {
         r.status = cst;

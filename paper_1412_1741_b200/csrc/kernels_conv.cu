@@ -355,6 +355,7 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
     uint64_t pt[kPark], ppos[kPark], pb0[kPark], pb1[kPark];
     uint32_t pe[kPark];
     uint32_t occ = 0;   // occupied slots (warp-uniform)
+    unsigned long long lk = 0;   // lookups at distinct states (warp-uniform; hdr->lookups)
     uint64_t tn = (uint64_t)blockIdx.x * kSetWarps + warp;
     const uint64_t tstride = (uint64_t)gridDim.x * kSetWarps;
     for (;;) {
@@ -390,6 +391,7 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
             while (D > 32 && pos < b1) {
                 const uint32_t colc = T.col(__ldg(in + pos));
                 uint32_t nD = 0;
+                lk += D;
                 if constexpr (OWN) {
                     // pass 1: image of every element, in place; owner tag of its state
                     for (uint32_t base = 0; base < D; base += 128) {
@@ -504,6 +506,7 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
             ppos[j] += cnt[j];
             uint32_t leaders;
             const uint32_t nd = distinct(pe[j], leaders);
+            lk += (unsigned long long)cnt[j] * nd;   // >= nd distinct states during these bytes
             if (nd <= dmax) {
                 write_handover(pt[j], ppos[j] - pb0[j], pe[j], leaders, nd);
                 occ &= ~(1u << j);
@@ -513,6 +516,7 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_set_kernel(const MatchPar
             }
         }
     }
+    if (lane == 0 && lk) atomicAdd(&P.hdr->lookups, lk);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -530,8 +534,49 @@ struct Follow {
     uint32_t e[CPT][kDMax], h[CPT][kDMax];
     uint32_t bad, A, wmask, K, K7F;   // K = (256 - A) per byte, K7F = K & 0x7F7F7F7F
     bool check;
+    // Per-lane merging (NEXT-2 (ii)): Dl = routes of chunk j still walked.  Once all routes
+    // of a chunk are in one state the lane walks route 0 only (Dl = 1) and keeps, in h[j][k],
+    // route k's hit OFFSET against route 0 at the meeting point; the predicated-off lookups
+    // issue no L1TEX wavefronts, which is what bounds the walk (the slowest lane of the
+    // warp no longer makes every lane pay kDMax lookups per byte).  finish() rebuilds.
+    uint32_t Dl[CPT];
+    uint32_t mv[CPT];   // 16-byte vectors walked with all D routes (stats: hdr->lookups)
 
     __device__ __forceinline__ Follow(const TT& t) : T(t) {}
+
+    // true when chunk j walks one route (now or already)
+    __device__ __forceinline__ bool lane_merge(int j, uint32_t vdone) {
+        if (Dl[j] > 1u) {
+            bool same = true;
+#pragma unroll
+            for (int k = 1; k < (int)kDMax; ++k) same &= (uint32_t)k >= Dl[j] || T.state(e[j][k]) == T.state(e[j][0]);
+            if (same) {
+#pragma unroll
+                for (int k = 1; k < (int)kDMax; ++k) h[j][k] -= h[j][0];   // u32 wrap-around is exact
+                Dl[j] = 1u;
+                mv[j] = vdone;
+            }
+        }
+        return Dl[j] <= 1u;
+    }
+    // lookups of chunk j over `bytes` bytes, `head` of them before the 16-byte vectors
+    __device__ __forceinline__ unsigned long long chunk_lookups(int j, uint64_t bytes, uint64_t head) const {
+        if (D[j] <= 1u) return bytes;
+        const uint64_t wide = mv[j] == 0xFFFFFFFFu ? bytes : min(bytes, head + (uint64_t)16 * mv[j]);
+        return bytes + (uint64_t)(D[j] - 1u) * wide;
+    }
+    __device__ __forceinline__ void finish() {
+#pragma unroll
+        for (int j = 0; j < CPT; ++j)
+            if (D[j] > 1u && Dl[j] == 1u) {
+#pragma unroll
+                for (int k = 1; k < (int)kDMax; ++k) {
+                    h[j][k] += h[j][0];
+                    e[j][k] = e[j][0];
+                }
+                Dl[j] = D[j];
+            }
+    }
 
     template <int K>
     __device__ __forceinline__ void word(int j, uint32_t w) {
@@ -547,7 +592,7 @@ struct Follow {
             const uint32_t colc = T.colm(__byte_perm(wm, 0u, 0x4440u | b));
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                if (K == 1 || (uint32_t)k < D[j]) {
+                if (K == 1 || (uint32_t)k < Dl[j]) {
                     e[j][k] = T.next(e[j][k], colc);
                     h[j][k] += T.hit(e[j][k]);
                 }
@@ -563,7 +608,6 @@ struct Follow {
     // vectors), then one route per chunk; the others are rebuilt at the end (rebuild()).
     static constexpr int PF = CPT == 1 ? 4 : 2;
     bool merged;
-    uint32_t e0[CPT], h0[CPT];
 
     __device__ __forceinline__ void run(uint32_t nvmax, bool multi) {
         merged = !multi;
@@ -604,31 +648,11 @@ struct Follow {
                     if ((vv & 3u) == 3u) {
                         bool conv = true;
 #pragma unroll
-                        for (int j = 0; j < CPT; ++j)
-#pragma unroll
-                            for (int k = 1; k < (int)kDMax; ++k)
-                                conv &= (uint32_t)k >= D[j] || T.state(e[j][k]) == T.state(e[j][0]);
-                        if (__all_sync(0xFFFFFFFFu, conv)) {
-                            merged = true;
-#pragma unroll
-                            for (int j = 0; j < CPT; ++j) {
-                                e0[j] = e[j][0];
-                                h0[j] = h[j][0];
-                            }
-                        }
+                        for (int j = 0; j < CPT; ++j) conv &= lane_merge(j, vv + 1u);
+                        if (__all_sync(0xFFFFFFFFu, conv)) merged = true;
                     }
                 }
             }
-        }
-        if (multi && merged) {   // rebuild the routes that were carried by route 0
-#pragma unroll
-            for (int j = 0; j < CPT; ++j)
-#pragma unroll
-                for (int k = 1; k < (int)kDMax; ++k)
-                    if ((uint32_t)k < D[j]) {
-                        h[j][k] = h[j][0] + (h[j][k] - h0[j]);   // u32 wrap-around is exact here
-                        e[j][k] = e[j][0];
-                    }
         }
     }
 
@@ -637,7 +661,7 @@ struct Follow {
         const uint32_t colc = T.col(c);
 #pragma unroll
         for (int k = 0; k < (int)kDMax; ++k)
-            if ((uint32_t)k < D[j]) {
+            if ((uint32_t)k < Dl[j]) {
                 e[j][k] = T.next(e[j][k], colc);
                 h[j][k] += T.hit(e[j][k]);
             }
@@ -645,7 +669,7 @@ struct Follow {
 };
 
 template <class TT, int CPT>
-__global__ void __launch_bounds__(1024) conv_follow_kernel(const MatchParams P) {
+__global__ void __launch_bounds__(kFollowThreads) conv_follow_kernel(const MatchParams P) {
     extern __shared__ __align__(16) unsigned char sm[];
     const DevDfa& d = P.d;
     TT T;
@@ -660,7 +684,7 @@ __global__ void __launch_bounds__(1024) conv_follow_kernel(const MatchParams P) 
     F.K = ((256u - d.A) & 0xFFu) * 0x01010101u;
     F.K7F = F.K & 0x7F7F7F7Fu;
     F.wmask = T.word_mask();
-    uint64_t t[CPT], a[CPT], b1[CPT];
+    uint64_t t[CPT], a[CPT], b1[CPT], a0[CPT], hdb[CPT];
     bool act[CPT];
     const uint64_t tb = (uint64_t)blockIdx.x * blockDim.x * CPT + threadIdx.x;
 #pragma unroll
@@ -672,6 +696,8 @@ __global__ void __launch_bounds__(1024) conv_follow_kernel(const MatchParams P) 
         b1[j] = live ? conv_b(P, t[j] + 1) : b0;
         const uint32_t D0 = live ? info->D : 0u;
         F.D[j] = D0 == kWide ? 0u : D0;   // follow only handed-over chunks
+        F.Dl[j] = F.D[j];
+        F.mv[j] = 0xFFFFFFFFu;
         act[j] = F.D[j] != 0;
         a[j] = act[j] ? b0 + info->m : b1[j];
 #pragma unroll
@@ -683,6 +709,8 @@ __global__ void __launch_bounds__(1024) conv_follow_kernel(const MatchParams P) 
         const uint64_t mis = act[j] ? (uint64_t)(((uintptr_t)(in + a[j])) & 15u) : 0u;
         uint64_t hd = mis ? a[j] + (16 - mis) : a[j];
         if (hd > b1[j]) hd = b1[j];
+        a0[j] = a[j];
+        hdb[j] = hd - a[j];
         for (; a[j] < hd; ++a[j]) F.step1(j, in[a[j]]);
         F.nv[j] = act[j] ? (uint32_t)((b1[j] - a[j]) >> 4) : 0u;
         F.p[j] = in + a[j];
@@ -706,6 +734,15 @@ __global__ void __launch_bounds__(1024) conv_follow_kernel(const MatchParams P) 
         a[j] += (uint64_t)F.nv[j] << 4;
         for (; act[j] && a[j] < b1[j]; ++a[j]) F.step1(j, in[a[j]]);
     }
+    {
+        unsigned long long lk = 0;
+#pragma unroll
+        for (int j = 0; j < CPT; ++j)
+            if (act[j]) lk += F.chunk_lookups(j, b1[j] - a0[j], hdb[j]);
+        lk = warp_sum(lk);
+        if ((threadIdx.x & 31u) == 0 && lk) atomicAdd(&P.hdr->lookups, lk);
+    }
+    F.finish();
     const bool anybad = (F.bad & 0x80808080u) != 0;
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
@@ -773,6 +810,8 @@ __global__ void __launch_bounds__(kFThreads) conv_follow_tma_kernel(const MatchP
     const uint64_t b0 = conv_b(P, t), b1 = live ? conv_b(P, t + 1) : b0;
     const uint32_t D0 = live ? info->D : 0u;
     F.D[0] = D0 == kWide ? 0u : D0;   // follow only handed-over chunks
+    F.Dl[0] = F.D[0];
+    F.mv[0] = 0xFFFFFFFFu;
     const bool act = F.D[0] != 0;
     const uint32_t m = act ? info->m : 0u;
 #pragma unroll
@@ -803,7 +842,6 @@ __global__ void __launch_bounds__(kFThreads) conv_follow_tma_kernel(const MatchP
     }
     const uint32_t Dw = __reduce_max_sync(0xFFFFFFFFu, staged ? F.D[0] : 0u);
     bool merged = Dw <= 1;
-    uint32_t e0 = 0, h0 = 0;
     if (warp_staged) {
         const uint32_t sw = (lane >> 1) & 3u, off = lane * kFBox;
         uint32_t slot = 0, phase = 0;
@@ -840,30 +878,22 @@ __global__ void __launch_bounds__(kFThreads) conv_follow_tma_kernel(const MatchP
                 phase ^= 1u;
             }
             if (!merged) {
-                bool conv = true;
-#pragma unroll
-                for (int k = 1; k < (int)kDMax; ++k)
-                    conv &= !staged || (uint32_t)k >= F.D[0] || T.state(F.e[0][k]) == T.state(F.e[0][0]);
-                if (__all_sync(0xFFFFFFFFu, conv)) {
-                    merged = true;
-                    e0 = F.e[0][0];
-                    h0 = F.h[0][0];
-                }
+                const bool conv = !staged || F.lane_merge(0, 4u * (s + 1u) > su ? 4u * (s + 1u) - su : 0u);
+                if (__all_sync(0xFFFFFFFFu, conv)) merged = true;
             }
         }
-        if (staged && Dw > 1 && merged) {   // rebuild the routes carried by route 0
-#pragma unroll
-            for (int k = 1; k < (int)kDMax; ++k)
-                if ((uint32_t)k < F.D[0]) {
-                    F.h[0][k] = F.h[0][0] + (F.h[0][k] - h0);   // u32 wrap-around is exact here
-                    F.e[0][k] = F.e[0][0];
-                }
-        }
-        (void)e0;
     }
     if (act && !staged) {   // the last chunk: from global memory, every route
         for (uint64_t a = b0 + m; a < b1; ++a) F.step1(0, in[a]);
     }
+    {
+        // staged rows: head = bytes up to the first staged 16-byte unit
+        const uint64_t bytes = act ? b1 - (b0 + m) : 0u;
+        unsigned long long lk = act ? F.chunk_lookups(0, bytes, staged ? min((uint64_t)su * 16u - (uint64_t)m, bytes) : bytes) : 0u;
+        lk = warp_sum(lk);
+        if (lane == 0 && lk) atomicAdd(&P.hdr->lookups, lk);
+    }
+    F.finish();
     if (!act) return;
     SurvRec& sr = W.surv[t];
     sr.n = F.D[0];
@@ -1031,14 +1061,14 @@ __global__ void conv_wide_kernel(const MatchParams P) {
 // merged) -- thread per chunk: head walk, survivor pick, validation, stats.
 template <bool W32>
 __global__ void __launch_bounds__(kFollowThreads) conv_map1_kernel(const MatchParams P) {
-    __shared__ unsigned long long acc[2];
+    __shared__ unsigned long long acc[3];
     const DevDfa& d = P.d;
-    if (threadIdx.x < 2) acc[threadIdx.x] = 0;
+    if (threadIdx.x < 3) acc[threadIdx.x] = 0;
     __syncthreads();
     const ConvWs W = conv_ws(P);
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t A = d.A;
-    unsigned long long rc = 0, steps = 0;
+    unsigned long long rc = 0, steps = 0, lkm = 0;
     if (t < P.p && !(P.hdr->err & 2u) && W.info[t].D != kWide && (t == 0 || W.ends[t - 1].n == 1)) {
         const uint64_t b0 = conv_b(P, t), b1 = conv_b(P, t + 1);
         const ConvChunk& c = W.info[t];
@@ -1064,17 +1094,21 @@ __global__ void __launch_bounds__(kFollowThreads) conv_map1_kernel(const MatchPa
             rc = route_count(P, cl, P.in[b0], __ldg(d.Lcnt + li));
         }
         steps = rc * (b1 - b0);
+        lkm = c.m;
     }
     rc = warp_sum(rc);
     steps = warp_sum(steps);
+    lkm = warp_sum(lkm);
     if ((threadIdx.x & 31u) == 0 && rc) {
         atomicAdd(acc + 0, rc);
         atomicAdd(acc + 1, steps);
+        atomicAdd(acc + 2, lkm);
     }
     __syncthreads();
     if (threadIdx.x == 0 && acc[0]) {
         atomicAdd(&P.hdr->routes, acc[0]);
         atomicAdd(&P.hdr->steps, acc[1]);
+        atomicAdd(&P.hdr->lookups, acc[2]);
     }
 }
 
@@ -1083,18 +1117,18 @@ __global__ void __launch_bounds__(kFollowThreads) conv_map1_kernel(const MatchPa
 template <bool SMEM, bool W32>
 __global__ void __launch_bounds__(kSetWarps * 32) conv_map_kernel(const MatchParams P) {
     extern __shared__ __align__(16) unsigned char sm[];
-    __shared__ unsigned long long acc[2];
+    __shared__ unsigned long long acc[3];
     const DevDfa& d = P.d;
     Tab<SMEM, W32> T;
     T.init(d, stage_table<SMEM, W32>(d, sm));
-    if (threadIdx.x < 2) acc[threadIdx.x] = 0;
+    if (threadIdx.x < 3) acc[threadIdx.x] = 0;
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const ConvWs W = conv_ws(P);
     const uint8_t* in = P.in;
     const uint32_t A = d.A;
     const bool skip = (P.hdr->err & 2u) != 0;   // wide chunks: the sequential fallback resolves
-    unsigned long long routes = 0, steps = 0;
+    unsigned long long routes = 0, steps = 0, lkw = 0;
     for (uint64_t t = (uint64_t)blockIdx.x * kSetWarps + warp; t < P.p && !skip; t += (uint64_t)gridDim.x * kSetWarps) {
         if (t == 0 || W.info[t].D == kWide) continue;   // wide: conv_wide_kernel's
         const uint32_t nin = W.ends[t - 1].n;
@@ -1138,16 +1172,19 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_map_kernel(const MatchPar
             const uint64_t rc = route_count(P, cl, in[b0], __ldg(d.Lcnt + li));
             routes += rc;
             steps += rc * (b1 - b0);
+            lkw += (unsigned long long)nin * c.m;
         }
     }
     if (lane == 0 && routes) {
         atomicAdd(acc + 0, routes);
         atomicAdd(acc + 1, steps);
+        atomicAdd(acc + 2, lkw);
     }
     __syncthreads();
     if (threadIdx.x == 0 && acc[0]) {
         atomicAdd(&P.hdr->routes, acc[0]);
         atomicAdd(&P.hdr->steps, acc[1]);
+        atomicAdd(&P.hdr->lookups, acc[2]);
     }
 }
 

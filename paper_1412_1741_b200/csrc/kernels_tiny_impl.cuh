@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
                 r.num_chunks = P.cpi;
                 r.routes = st[1];
                 r.route_steps = st[2];
-                r.reserved = 0;
+                r.lookups_k = 0;
                 r.status = st[0] ? PAREM_ESYMBOL : PAREM_OK;
                 r.bad_offset = st[0] ? ~st[0] : 0ull;
                 P.results[b] = r;

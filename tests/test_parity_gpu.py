@@ -316,6 +316,12 @@ def test_conv_configs(parem, torch_mod, k, L):
             b = oracle.grid_boundaries(x.size, L)
             assert got.num_chunks == len(b) - 1
             assert (got.routes, got.route_steps) == oracle.route_stats(c.table, x, b)
+        if cand == "parem" and L >= 4096:
+            # executed lookups (parem_result.lookups_k, units of 1024): every byte is walked at
+            # least once (set walk or follow), and merging never costs more than walking every
+            # candidate over its whole chunk (the paper's route_steps) plus the join's head walks
+            assert x.size <= got.lookups <= got.route_steps + 32 * x.size, got
+            assert got.lookups < got.route_steps // 4, got   # routes merge early on these DFAs
 
 
 @pytest.mark.parametrize("seed", range(40))
