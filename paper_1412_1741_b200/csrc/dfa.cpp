@@ -207,6 +207,7 @@ extern "C" int parem_dfa_create(uint32_t Q, uint32_t A, const void* table, uint3
     // ---- convergence probe for the converging path (kernels_conv.cu): the set walk
     // delta*(Q, w) under seeded uniform symbols; how many steps until <= 4 / 1 states ----
     uint32_t conv_t4 = 0, conv_t1 = 0;
+    uint64_t conv_work4 = 0;   // sum of set sizes until <= 4 states: the set walk's lookups per chunk
     if (!tiny && !has_sink) {
         std::vector<uint32_t> cur(Qp), nxt;
         std::vector<uint32_t> mark(Qp, 0);
@@ -232,7 +233,10 @@ extern "C" int parem_dfa_create(uint32_t Q, uint32_t A, const void* table, uint3
                 }
             }
             cur.swap(nxt);
-            if (!conv_t4 && cur.size() <= 4) conv_t4 = t;
+            if (!conv_t4 && cur.size() <= 4) {
+                conv_t4 = t;
+                conv_work4 = work;
+            }
             if (cur.size() == 1) conv_t1 = t;
         }
     }
@@ -263,6 +267,7 @@ extern "C" int parem_dfa_create(uint32_t Q, uint32_t A, const void* table, uint3
     h->num_sms = sms;
     h->conv_t4 = conv_t4;
     h->conv_t1 = conv_t1;
+    h->conv_work4 = conv_work4;
     *out = h;
     return PAREM_OK;
 }

@@ -139,6 +139,7 @@ struct parem_dfa {
     // create-time convergence probe (set walk from all of Q under seeded uniform symbols):
     // steps until <= 4 / exactly 1 distinct states remain (0 = not within the probe)
     uint32_t conv_t4, conv_t1;
+    uint64_t conv_work4;
 };
 
 namespace parem {

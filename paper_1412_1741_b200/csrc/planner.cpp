@@ -181,6 +181,7 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         }
         if (const char* e = getenv("PAREM_SET_OWN")) plan->set_own = (uint32_t)atoi(e);
         plan->conv_fthreads = 512;
+        if (const char* e = getenv("PAREM_CONV_FTHREADS")) plan->conv_fthreads = (uint32_t)atoi(e);   // experiments
         plan->conv_cpt = 1;
         plan->conv_swarps = conv_swarps;
         if (const char* e = getenv("PAREM_CONV_CPT")) plan->conv_cpt = atoi(e) == 2 ? 2 : 1;
@@ -189,7 +190,18 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         // second wave or unevenly loaded SMs cost more than the extra chains bring); the
         // follow is bound by shared-memory bank conflicts (smem tables) or L1TEX gather
         // wavefronts (L2 tables), not by latency, and more chunks only add set-walk work
-        uint64_t chains = (uint64_t)sms * (plan->conv_tma ? 1024 : 512);
+        // ... unless the set walk of one chunk (create-time probe: conv_work4 lookups until
+        // <= 4 states) costs about as much as following the chunk itself: slowly converging
+        // automata (cfg4: ~60 k set-walk lookups against 28 KB chunks) run fewer, longer
+        // chunks -- their follow keeps several routes per lane in flight and loses little
+        // (cfg4, chains/SM 256 / 320 / 384 / 448 / 512: 22.5 / 21.8 / 23.3 / 24.1 / 26.0 ms per
+        // step; cfg5, where the set walk is cheap: 27.4 / 22.9 / 20.1 / 18.4 / 17.3 ms)
+        if (!plan->conv_tma && !getenv("PAREM_CONV_FTHREADS")) {
+            const double L512 = (double)n / (512.0 * sms);
+            const double rho = L512 > 0 ? (double)dfa->conv_work4 / L512 : 0.0;
+            plan->conv_fthreads = rho >= 1.5 ? 320 : rho >= 0.75 ? 416 : 512;
+        }
+        uint64_t chains = (uint64_t)sms * (plan->conv_tma ? 1024 : plan->conv_fthreads);
         uint32_t dmax = 4;
         uint64_t headx = 16;
         if (const char* e = getenv("PAREM_CONV_CHAINS")) chains = strtoull(e, nullptr, 10);   // experiments
