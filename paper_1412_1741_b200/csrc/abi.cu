@@ -11,6 +11,8 @@
 #include <utility>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only; a no-op unless a tool (nsys, ncu --nvtx) is attached
+
 #include "kernels_common.cuh"
 
 namespace parem {
@@ -101,6 +103,14 @@ void prof_after(const char* name, cudaStream_t s) {
     p.last = e;
 }
 
+// NVTX range over the host side of one ABI call (tracing)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 static int match_impl(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, uint64_t offset_base, void* d_ws,
                       size_t ws_bytes, const parem_options* opts, const parem_result* d_carry,
                       parem_result* d_result, cudaStream_t stream, uint64_t* d_positions = nullptr,
@@ -152,6 +162,10 @@ static int match_impl(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, 
         }
     }
     prof_begin(stream);
+    static const char* const kRangeNames[2][4] = {
+        {"parem_match:trivial", "parem_match:tiny", "parem_match:lanes", "parem_match:conv"},
+        {"parem_find:trivial", "parem_find:tiny", "parem_find:lanes", "parem_find:conv"}};
+    NvtxRange range(kRangeNames[find ? 1 : 0][plan.kernel & 3u]);
     if (plan.kernel == kKernelTrivial) return launch_trivial(P, stream);
     if (find) {
         find_bind(plan, P, reinterpret_cast<unsigned char*>(d_ws) + ((plan.ws + 255) & ~(size_t)255));
@@ -256,6 +270,7 @@ extern "C" size_t parem_batch_workspace_bytes(const parem_dfa* dfa, uint64_t n, 
 extern "C" int parem_match_batch_async(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, uint64_t count,
                                        void* d_ws, size_t ws_bytes, const parem_options* opts,
                                        parem_result* d_results, void* stream_) {
+    NvtxRange nvtx_range("parem_match_batch");
     set_error("");
     cudaStream_t stream = (cudaStream_t)stream_;
     if (!dfa || !d_results || (count && n && !d_input)) { set_error("null argument"); return PAREM_EINVAL; }
@@ -301,6 +316,7 @@ extern "C" int parem_match_batch_async(const parem_dfa* dfa, const uint8_t* d_in
 extern "C" int parem_segment_map(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, int32_t prev_symbol,
                                  const parem_options* opts, parem_segmap_entry* h_map, int32_t* status,
                                  uint64_t* bad_offset, void* stream_) {
+    NvtxRange nvtx_range("parem_segment_map");
     set_error("");
     if (!dfa || !h_map || !status || !bad_offset || (n && !d_input)) { set_error("null argument"); return PAREM_EINVAL; }
     cudaStream_t stream = (cudaStream_t)stream_;
@@ -513,6 +529,7 @@ cudaError_t host_pipe(HostPipe** out) {
 
 extern "C" int parem_match_host(const parem_dfa* dfa, const uint8_t* h_input, uint64_t n, const parem_options* opts,
                                 parem_result* h_result, void* stream_) {
+    NvtxRange nvtx_range("parem_match_host");
     if (!h_result || !dfa || (n && !h_input)) { set_error("null argument"); return PAREM_EINVAL; }
     cudaStream_t stream = (cudaStream_t)stream_;
     // segments: 64 MiB for the tiny kernel; 512 MiB for the large-DFA paths, whose per-match

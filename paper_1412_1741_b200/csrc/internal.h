@@ -115,6 +115,7 @@ struct Plan {
     uint32_t dmax;           // conv: set-walk hand-over threshold (1, 2 or 4 survivors)
     uint32_t conv_tma;       // conv: TMA-staged follow walk (rows of L bytes)
     uint32_t conv_rep;       // conv: follow table replicated in R = 8 / 16 copies (0: plain)
+    uint32_t conv_hyb;       // conv: hybrid follow table (packed columns in shared memory + L2)
     uint32_t set_own;        // conv: phase-A dedup by owner tags (Qpad <= 1024)
     uint32_t conv_cpt;       // conv: chunks per follow thread (1 or 2)
     uint32_t conv_fthreads;  // conv: follow block size
@@ -163,6 +164,7 @@ size_t find_extra_bytes(const Plan& plan, const DevDfa& d);
 void find_bind(const Plan& plan, MatchParams& P, unsigned char* extra);
 size_t conv_ws_total(uint64_t p);
 size_t conv_rep_smem(const DevDfa& d, uint32_t R);        // 0 if the layout does not apply
+bool conv_hybrid_applies(const DevDfa& d);
 size_t conv_follow_tma_smem(size_t table_bytes);
 size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap, uint32_t warps);
 int launch_trivial(const MatchParams& P, cudaStream_t s);

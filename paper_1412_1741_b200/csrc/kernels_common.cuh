@@ -104,7 +104,21 @@ __device__ __forceinline__ uint32_t route_count(const MatchParams& P, uint32_t c
 
 // First offset in [a, b) holding a byte >= A (slow path, only after a detection).
 __device__ __forceinline__ uint64_t first_bad(const uint8_t* in, uint64_t a, uint64_t b, uint32_t A) {
-    for (uint64_t k = a; k < b; ++k)
+    if (A >= 256u) return b;   // every byte is a symbol
+    uint64_t k = a;
+    for (; k < b && (((uintptr_t)(in + k)) & 15u); ++k)
+        if (in[k] >= A) return k;
+    // 16 bytes at a time: byte x >= A iff x + (256 - A) carries out of bit 7
+    const uint32_t K = (256u - A) * 0x01010101u, K7 = K & 0x7F7F7F7Fu;
+    for (; k + 16 <= b; k += 16) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(in + k));
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        uint32_t bad = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) bad |= (w[q] & K) | ((w[q] | K) & ((w[q] & 0x7F7F7F7Fu) + K7));
+        if (bad & 0x80808080u) break;   // the byte loop below finds the offset
+    }
+    for (; k < b; ++k)
         if (in[k] >= A) return k;
     return b;
 }

@@ -135,7 +135,7 @@ __host__ __device__ __forceinline__ size_t tab_bytes(const DevDfa& d) {
 template <bool SMEM, bool W32>
 struct Tab {
     static constexpr uint32_t ES = W32 ? 4 : 2, ACC = W32 ? 31 : 15;
-    static constexpr bool kSmem = SMEM, kW32 = W32, kRep = false;
+    static constexpr bool kSmem = SMEM, kW32 = W32, kRep = false, kHyb = false;
     const unsigned char* g;
     uint32_t cbase, COL, SMASK, CMASK;
 
@@ -206,7 +206,7 @@ __host__ __device__ __forceinline__ uint32_t rep_col_bytes(uint32_t Qpad, uint32
 template <int R>
 struct TabR {
     static constexpr uint32_t ES = 2;
-    static constexpr bool kSmem = true, kW32 = false, kRep = true;
+    static constexpr bool kSmem = true, kW32 = false, kRep = true, kHyb = false;
     static constexpr int kR = R;
     uint32_t tbase, COL, FMASK, AM1, k;
 
@@ -262,15 +262,109 @@ __host__ __device__ __forceinline__ size_t rep_smem_bytes(const DevDfa& d, uint3
     return col > (1u << 15) ? 0 : (size_t)d.A * col + col;   // + alignment slack
 }
 
+// Hybrid table for the follow walk of tables that do not fit shared memory (cfg5: 1024 x 256,
+// 512 KiB): the first CS symbol columns live in shared memory, PACKED three 10-bit states per
+// word (WPC = ceil(Qpad / 3) words per column), the other columns are read from the u16 table
+// in global memory (L1/L2).  The selection is branch-free: a lane served from shared memory
+// aims its global load at entry 0 (one shared wavefront for all such lanes), a lane served
+// from global memory aims its shared load at word 0 (a broadcast); ptxas turns a per-lane
+// LDS/LDG choice into a divergent branch, which was 2x slower (profiles/r02_conv_sweeps.txt,
+// g25).  Accept flags come from a Qpad-bit bitmap in shared memory (the packed entries have
+// no room for them).  The L2 gather rate bounds the all-global walk (~1.1 lookups/clk/SM,
+// tools/follow_probe.cu); with 144 of 256 columns in shared memory and two chunks per
+// thread the probe reaches 1.7 (profiles/r02_follow_probe.txt).
+struct TabH {
+    static constexpr bool kSmem = true, kW32 = false, kRep = false, kHyb = true;
+    static constexpr uint32_t kBudget = 192u * 1024u;   // more starves the L1 the input stream needs
+    const uint16_t* g;
+    uint32_t sbase, abase, CS, WPC, Qpad, AM1, CMASK;
+
+    __host__ __device__ static uint32_t wpc(uint32_t Qpad) { return (Qpad + 2u) / 3u; }
+    __host__ __device__ static uint32_t columns(const DevDfa& d) {
+        const uint32_t c = (kBudget - d.Qpad / 8u - 32u) / (wpc(d.Qpad) * 4u);
+        return c < d.A ? c : d.A;
+    }
+    __host__ __device__ static bool applies(const DevDfa& d) {
+        // u16 table, 10-bit states, and enough columns on chip to matter
+        return !d.lanes_u32 && d.Qpad <= 1024u && 5u * columns(d) >= 2u * d.A;
+    }
+    __host__ __device__ static size_t bytes(const DevDfa& d) {
+        return (size_t)columns(d) * wpc(d.Qpad) * 4u + d.Qpad / 8u + 32u;
+    }
+    __device__ __forceinline__ void init(const DevDfa& d, unsigned char* sm) {
+        g = reinterpret_cast<const uint16_t*>(d.lanes_tab);
+        CS = columns(d);
+        WPC = wpc(d.Qpad);
+        Qpad = d.Qpad;
+        AM1 = d.A - 1u;
+        CMASK = d.Apad - 1u;
+        uint32_t* pw = reinterpret_cast<uint32_t*>(sm);
+        sbase = smem_u32(pw);
+        for (uint32_t i = threadIdx.x; i < CS * WPC; i += blockDim.x) {
+            const uint32_t c = i / WPC, q = i - c * WPC;
+            uint32_t w = 0;
+#pragma unroll
+            for (uint32_t r = 0; r < 3; ++r) {
+                const uint32_t st = 3u * q + r;
+                if (st < Qpad) w |= (((uint32_t)__ldg(g + (size_t)c * Qpad + st) & 0x7FFFu) >> 1) << (10u * r);
+            }
+            pw[i] = w;
+        }
+        uint32_t* aw = pw + CS * WPC;
+        abase = smem_u32(aw);
+        for (uint32_t i = threadIdx.x; i < (Qpad + 31u) / 32u; i += blockDim.x) {
+            uint32_t w = 0;
+            for (uint32_t b = 0; b < 32u; ++b) {
+                const uint32_t st = 32u * i + b;
+                if (st < d.Qp && d.acc[st]) w |= 1u << b;
+            }
+            aw[i] = w;
+        }
+    }
+    __device__ __forceinline__ uint32_t col(uint32_t c) const { return min(c, AM1); }
+    __device__ __forceinline__ uint32_t colm(uint32_t c) const { return c; }   // c <= CMASK < Apad
+    // e = state | accept << 31
+    __device__ __forceinline__ uint32_t next(uint32_t e, uint32_t c) const {
+        const uint32_t st = e & 0x3FFu;
+        const bool insm = c < CS;
+        const uint32_t q = (st * 43691u) >> 17, r = st - 3u * q;
+        const uint32_t vg = __ldg(g + (insm ? 0u : c * Qpad + st));
+        uint32_t ww, aw;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(ww) : "r"(sbase + 4u * (insm ? c * WPC + q : 0u)));
+        const uint32_t dst = insm ? (ww >> (r * 10u)) & 0x3FFu : (vg & 0x7FFu) >> 1;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(aw) : "r"(abase + ((dst >> 5) << 2)));
+        return dst | (((aw >> (dst & 31u)) & 1u) << 31);
+    }
+    // the same lookup for a route that may be switched off: a dead route aims both loads at
+    // the dummy addresses (no extra wavefronts) and its result is ignored by the caller --
+    // keeps the multi-route walk free of branches
+    __device__ __forceinline__ uint32_t next_live(uint32_t e, uint32_t c, bool live) const {
+        const uint32_t st = e & 0x3FFu;
+        const bool insm = c < CS;
+        const uint32_t q = (st * 43691u) >> 17, r = st - 3u * q;
+        const uint32_t vg = __ldg(g + ((live && !insm) ? c * Qpad + st : 0u));
+        uint32_t ww, aw;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(ww) : "r"(sbase + 4u * ((live && insm) ? c * WPC + q : 0u)));
+        const uint32_t dst = insm ? (ww >> (r * 10u)) & 0x3FFu : (vg & 0x7FFu) >> 1;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(aw) : "r"(abase + ((dst >> 5) << 2)));
+        return dst | (((aw >> (dst & 31u)) & 1u) << 31);
+    }
+    __device__ __forceinline__ uint32_t state(uint32_t e) const { return e & 0x3FFu; }
+    __device__ __forceinline__ uint32_t hit(uint32_t e) const { return e >> 31; }
+    __device__ __forceinline__ uint32_t start(uint32_t s) const { return s; }
+    __device__ __forceinline__ uint32_t word_mask() const { return CMASK * 0x01010101u; }
+};
+
 // staging and footprint of any follow table type
 template <class TT>
 __device__ __forceinline__ void tab_setup(TT& T, const DevDfa& d, unsigned char* sm) {
-    if constexpr (TT::kRep) T.init(d, sm);
+    if constexpr (TT::kRep || TT::kHyb) T.init(d, sm);
     else T.init(d, stage_table<TT::kSmem, TT::kW32>(d, sm));
 }
 template <class TT>
 __host__ __device__ __forceinline__ size_t tab_smem(const DevDfa& d) {
-    if constexpr (TT::kRep) return rep_smem_bytes(d, TT::kR);
+    if constexpr (TT::kHyb) return TT::bytes(d);
+    else if constexpr (TT::kRep) return rep_smem_bytes(d, TT::kR);
     else return smem_tab_bytes(d, TT::kSmem);
 }
 
@@ -559,6 +653,44 @@ struct Follow {
         }
         return Dl[j] <= 1u;
     }
+    // One 32-bit word of EVERY chunk of the thread, byte by byte with the chunks interleaved
+    // (b -> j -> k): the CPT chains of a thread overlap their lookups (issue is in order, so
+    // walking chunk 0's sixteen bytes before chunk 1's would serialise them).  Hybrid tables
+    // use the switched lookup (no branch per route); on[j] = chunk j has this vector.
+    template <int K>
+    __device__ __forceinline__ void words(const uint32_t (&w)[CPT], const bool (&on)[CPT]) {
+        uint32_t wm[CPT];
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+            if (check && on[j]) {
+                const uint32_t t = (w[j] & 0x7F7F7F7Fu) + K7F;
+                bad |= (w[j] & this->K) | ((w[j] | this->K) & t);
+            }
+            wm[j] = w[j] & wmask;
+        }
+#pragma unroll
+        for (uint32_t b = 0; b < 4; ++b) {
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) {
+                const uint32_t colc = T.colm(__byte_perm(wm[j], 0u, 0x4440u | b));
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const bool live = on[j] && (K == 1 || (uint32_t)k < Dl[j]);
+                    if constexpr (TT::kHyb) {
+                        const uint32_t ne = T.next_live(e[j][k], colc, live);
+                        e[j][k] = live ? ne : e[j][k];
+                        h[j][k] += live ? T.hit(ne) : 0u;
+                    } else {
+                        if (live) {
+                            e[j][k] = T.next(e[j][k], colc);
+                            h[j][k] += T.hit(e[j][k]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+
     // lookups of chunk j over `bytes` bytes, `head` of them before the 16-byte vectors
     __device__ __forceinline__ unsigned long long chunk_lookups(int j, uint64_t bytes, uint64_t head) const {
         if (D[j] <= 1u) return bytes;
@@ -627,7 +759,29 @@ struct Follow {
                     x[j] = ring[j][u];
                     if (vv + PF < nv[j]) ring[j][u] = ldg_v4_na(p[j] + 16ull * (vv + PF));
                 }
-                if (merged) {
+                if constexpr (CPT > 1 || TT::kHyb) {
+                    bool on[CPT];
+                    uint32_t w0[CPT], w1[CPT], w2[CPT], w3[CPT];
+#pragma unroll
+                    for (int j = 0; j < CPT; ++j) {
+                        on[j] = vv < nv[j];
+                        w0[j] = x[j].x;
+                        w1[j] = x[j].y;
+                        w2[j] = x[j].z;
+                        w3[j] = x[j].w;
+                    }
+                    if (merged) {
+                        words<1>(w0, on);
+                        words<1>(w1, on);
+                        words<1>(w2, on);
+                        words<1>(w3, on);
+                    } else {
+                        words<kDMax>(w0, on);
+                        words<kDMax>(w1, on);
+                        words<kDMax>(w2, on);
+                        words<kDMax>(w3, on);
+                    }
+                } else if (merged) {
 #pragma unroll
                     for (int j = 0; j < CPT; ++j)
                         if (vv < nv[j]) {
@@ -645,6 +799,8 @@ struct Follow {
                             word<kDMax>(j, x[j].z);
                             word<kDMax>(j, x[j].w);
                         }
+                }
+                if (!merged) {
                     if ((vv & 3u) == 3u) {
                         bool conv = true;
 #pragma unroll
@@ -669,7 +825,7 @@ struct Follow {
 };
 
 template <class TT, int CPT>
-__global__ void __launch_bounds__(kFollowThreads) conv_follow_kernel(const MatchParams P) {
+__global__ void __launch_bounds__(kFollowThreads, 1) conv_follow_kernel(const MatchParams P) {
     extern __shared__ __align__(16) unsigned char sm[];
     const DevDfa& d = P.d;
     TT T;
@@ -1379,7 +1535,10 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
         else if (plan.conv_rep == 16) e = launch_follow_cpt<TabR<16>>(plan, P, rep_smem_bytes(d, 16), s);
         else e = launch_follow_cpt<Tab<SMEM, W32>>(plan, P, tb, s);
     } else {
-        e = launch_follow_cpt<Tab<SMEM, W32>>(plan, P, tb, s);
+        if (plan.conv_hyb && !W32 && TabH::applies(d))
+            e = plan.conv_cpt == 2 ? launch_follow<TabH, 2>(plan, P, TabH::bytes(d), s)
+                                   : launch_follow<TabH, 1>(plan, P, TabH::bytes(d), s);
+        else e = launch_follow_cpt<Tab<SMEM, W32>>(plan, P, tb, s);
     }
     prof_after("conv_follow", s);
     if (e != cudaSuccess) {
@@ -1426,6 +1585,7 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
 size_t conv_ws_total(uint64_t p) { return conv_ws_bytes(p); }
 
 size_t conv_rep_smem(const DevDfa& d, uint32_t R) { return rep_smem_bytes(d, R); }
+bool conv_hybrid_applies(const DevDfa& d) { return TabH::applies(d); }
 size_t conv_follow_tma_smem(size_t table_bytes) { return follow_tma_smem(table_bytes); }
 
 size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap, uint32_t warps) {

@@ -196,12 +196,20 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         // chunks -- their follow keeps several routes per lane in flight and loses little
         // (cfg4, chains/SM 256 / 320 / 384 / 448 / 512: 22.5 / 21.8 / 23.3 / 24.1 / 26.0 ms per
         // step; cfg5, where the set walk is cheap: 27.4 / 22.9 / 20.1 / 18.4 / 17.3 ms)
+        // Hybrid follow table (tables beyond shared memory with <= 1024 states: part of the
+        // columns packed in shared memory): faster per lookup but latency-bound at 512
+        // chains per SM, so two chunks per thread (1024 chains per SM).  Experimental knob
+        // first: PAREM_CONV_HYB=1.
+        plan->conv_hyb = 0;
+        if (const char* e = getenv("PAREM_CONV_HYB")) plan->conv_hyb = (uint32_t)atoi(e);
+        if (plan->conv_hyb && (conv_smem_tab || !conv_hybrid_applies(d) || plan->conv_tma)) plan->conv_hyb = 0;
+        if (plan->conv_hyb && !getenv("PAREM_CONV_CPT")) plan->conv_cpt = 2;
         if (!plan->conv_tma && !getenv("PAREM_CONV_FTHREADS")) {
             const double L512 = (double)n / (512.0 * sms);
             const double rho = L512 > 0 ? (double)dfa->conv_work4 / L512 : 0.0;
             plan->conv_fthreads = rho >= 1.5 ? 320 : rho >= 0.75 ? 416 : 512;
         }
-        uint64_t chains = (uint64_t)sms * (plan->conv_tma ? 1024 : plan->conv_fthreads);
+        uint64_t chains = (uint64_t)sms * (plan->conv_tma ? 1024 : plan->conv_fthreads * plan->conv_cpt);
         uint32_t dmax = 4;
         uint64_t headx = 16;
         if (const char* e = getenv("PAREM_CONV_CHAINS")) chains = strtoull(e, nullptr, 10);   // experiments

@@ -213,6 +213,82 @@ __global__ void __launch_bounds__(512) pkg(const uint32_t* __restrict__ ptab, ui
     if (e + h == sink[1]) sink[0] = e;
 }
 
+// packed hybrid fed by the real input stream: thread-per-chain 16-byte loads (no L1 allocation),
+// PF vectors in flight per chain -- does the small L1 left beside a 128-192 KiB table starve it?
+template <int C, int PF>
+__global__ void __launch_bounds__(512) pk_in(const uint16_t* __restrict__ tab, const uint32_t* __restrict__ ptab, uint32_t CS,
+                                              const uint8_t* __restrict__ in, uint64_t L, uint32_t nvec, uint32_t* sink) {
+    extern __shared__ __align__(16) uint32_t ps[];
+    for (uint32_t i = threadIdx.x; i < CS * 342u; i += blockDim.x) ps[i] = ptab[i];
+    __syncthreads();
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t e[C], h[C];
+    const uint8_t* p[C];
+    uint4 ring[C][PF];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+        e[k] = (uint32_t)(tid * 2654435761u + 977u * k) & 1023u;
+        h[k] = 0;
+        p[k] = in + (tid * C + k) * L;
+#pragma unroll
+        for (int u = 0; u < PF; ++u) ring[k][u] = ld_na(p[k] + 16 * u);
+    }
+    for (uint32_t v = 0; v < nvec; v += PF) {
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            uint32_t w[C][4];
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                const uint4 x = ring[k][u];
+                w[k][0] = x.x; w[k][1] = x.y; w[k][2] = x.z; w[k][3] = x.w;
+                if (v + u + PF < nvec) ring[k][u] = ld_na(p[k] + 16ull * (v + u + PF));
+            }
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4)
+#pragma unroll
+                for (uint32_t b = 0; b < 4; ++b)
+#pragma unroll
+                    for (int k = 0; k < C; ++k) {
+                        const uint32_t c = __byte_perm(w[k][q4], 0u, 0x4440u | b), st = e[k];
+                        const bool insm = c < CS;
+                        const uint32_t q = (st * 43691u) >> 17, r = st - 3u * q;
+                        const uint32_t vg = __ldg(tab + (insm ? 0u : c * 1024u + st));
+                        const uint32_t ww = ps[insm ? c * 342u + q : 0u];
+                        const uint32_t vs = (ww >> (r * 10u)) & 1023u;
+                        e[k] = insm ? vs : (vg & 1023u);
+                        h[k] += e[k] < 100u;
+                    }
+        }
+    }
+    uint32_t a = 0;
+#pragma unroll
+    for (int k = 0; k < C; ++k) a ^= e[k] + h[k];
+    if (a == sink[1]) sink[0] = a;
+}
+
+template <int C, int PF>
+static void run_pk_in(const uint16_t* tab, const uint32_t* ptab, uint32_t CS, const uint8_t* in, uint64_t nin, int sms, uint32_t* sink, double ghz) {
+    const size_t smem = (size_t)CS * 342 * 4 + 16;
+    CK(cudaFuncSetAttribute(pk_in<C, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const uint64_t chains = (uint64_t)sms * 512 * C;
+    uint64_t L = nin / chains;
+    if (L > 16384) L = 16384;
+    L &= ~(uint64_t)63;
+    if (L % 128 == 0) L -= 16;
+    const uint32_t nvec = (uint32_t)(L / 16) / PF * PF;
+    pk_in<C, PF><<<sms, 512, smem>>>(tab, ptab, CS, in, L, nvec, sink);
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaEventRecord(a);
+    pk_in<C, PF><<<sms, 512, smem>>>(tab, ptab, CS, in, L, nvec, sink);
+    cudaEventRecord(b); CK(cudaEventSynchronize(b));
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    const double lk = (double)chains * nvec * 16;
+    printf("packed+input CS %3u (%3zu KiB smem) thr/SM 512 C %d PF %d : %.3f Tlookup/s  %.2f lookups/clk/SM\n", CS, smem / 1024, C, PF,
+           lk / (ms * 1e-3) / 1e12, lk / (ms * 1e-3) / (sms * ghz * 1e9));
+    fflush(stdout);
+}
+
 static uint64_t splitmix(uint64_t& s) {
     uint64_t z = (s += 0x9E3779B97F4A7C15ull);
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -362,6 +438,12 @@ int main() {
             float ms; cudaEventElapsedTime(&ms, a, b);
             const double lk = (double)sms * tps * steps;
             printf("packed global (342 KiB) thr/SM %4d : %.3f Tlookup/s  %.2f lookups/clk/SM\n", tps, lk / (ms * 1e-3) / 1e12, lk / (ms * 1e-3) / (sms * ghz * 1e9));
+        }
+        for (uint32_t CS : {0u, 96u, 128u, 144u}) {
+            run_pk_in<1, 4>(tab, ptab, CS, in, nin, sms, sink, ghz);
+            run_pk_in<2, 2>(tab, ptab, CS, in, nin, sms, sink, ghz);
+            run_pk_in<2, 4>(tab, ptab, CS, in, nin, sms, sink, ghz);
+            run_pk_in<3, 2>(tab, ptab, CS, in, nin, sms, sink, ghz);
         }
         for (uint32_t CS : {0u, 144u}) {
             const size_t smem = (size_t)CS * 342 * 4 + 16;
