@@ -258,6 +258,20 @@ int parem_find_async(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, v
                      const parem_options* opts, uint64_t* d_positions, uint64_t max_positions,
                      parem_result* d_result, void* stream);
 
+/* ---- route trace (Alg. 1's visited-state vector Rr; Table II
+ * "Visited states") ----
+ * parem_trace_async runs the match (same d_result) and writes the states VISITED by the routes the
+ * join selects -- the concatenation of the Rr vectors of the true route of every chunk, which
+ * is the sequential run q_1 .. q_n -- for the window lo <= k < hi <= n:
+ *     d_states[k - lo] = state after symbol k   (uint32; PAREM_DEAD once the walk has died).
+ * d_states is device memory, caller-owned, hi - lo entries; lo == hi writes nothing.  Every
+ * chunk's true entering state is resolved as for parem_find_async and the chunks that meet the
+ * window are walked once more from it.  Workspace: parem_find_workspace_bytes.  On an ESYMBOL
+ * result the trace is unspecified.  EINVAL if lo > hi or hi > n. */
+int parem_trace_async(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, void* d_ws, size_t ws_bytes,
+                      const parem_options* opts, uint64_t lo, uint64_t hi, uint32_t* d_states,
+                      parem_result* d_result, void* stream);
+
 /* ---- regular-expression front end (host) ----
  * Compiles a pattern of the paper's language (Table III): concatenation `ab`,
  * Kleene star `a*`, union `a|b`, positive closure `a+`, range `[x..y]` (every alphabet

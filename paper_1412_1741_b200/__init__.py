@@ -381,6 +381,33 @@ class Dfa:
         r = MatchResult.from_bytes(res.cpu().numpy().tobytes()[:56])
         return r, pos[: min(cap, r.match_count)]
 
+    def trace_async(self, x, ws, lo: int, hi: int, states, result, opts=None, stream=None) -> None:
+        """Enqueue parem_trace_async: the match plus the visited states q_{k+1}, lo <= k < hi,
+        into the CUDA int32/uint32 tensor ``states`` (hi - lo entries)."""
+        x = _cuda_u8(x)
+        if states.numel() < hi - lo:
+            raise ValueError("states tensor smaller than the window")
+        st = self._L.parem_trace_async(self._h, C.c_void_p(x.data_ptr()), x.numel(), C.c_void_p(ws.data_ptr()),
+                                       ws.numel(), C.byref(opts) if opts is not None else None, int(lo), int(hi),
+                                       C.c_void_p(states.data_ptr()) if hi > lo else None,
+                                       C.c_void_p(result.data_ptr()), _stream(stream))
+        if st != PAREM_OK:
+            _err(self._L, st)
+
+    def trace(self, x, lo: int = 0, hi: int | None = None, opts=None):
+        """Synchronous route trace (Alg. 1's Rr of the selected routes): (MatchResult, CUDA int64
+        tensor of the states after symbols lo .. hi-1; PAREM_DEAD = 0xFFFFFFFF after death)."""
+        import torch
+
+        x = _cuda_u8(x)
+        hi = x.numel() if hi is None else int(hi)
+        ws = torch.zeros(self.find_workspace_bytes(x.numel(), opts), dtype=torch.uint8, device=x.device)
+        st = torch.empty(max(hi - lo, 1), dtype=torch.int32, device=x.device)
+        res = torch.zeros(64, dtype=torch.uint8, device=x.device)
+        self.trace_async(x, ws, lo, hi, st, res, opts)
+        r = MatchResult.from_bytes(res.cpu().numpy().tobytes()[:56])
+        return r, (st[: max(hi - lo, 0)].to(torch.int64) & 0xFFFFFFFF)
+
     def match_continue_async(self, x, offset_base: int, ws, carry, result, opts=None, stream=None) -> None:
         x = _cuda_u8(x)
         st = self._L.parem_match_continue_async(

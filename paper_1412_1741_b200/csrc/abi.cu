@@ -114,7 +114,8 @@ struct NvtxRange {
 static int match_impl(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, uint64_t offset_base, void* d_ws,
                       size_t ws_bytes, const parem_options* opts, const parem_result* d_carry,
                       parem_result* d_result, cudaStream_t stream, uint64_t* d_positions = nullptr,
-                      uint64_t max_positions = 0, bool find = false) {
+                      uint64_t max_positions = 0, bool find = false, uint32_t* d_trace = nullptr, uint64_t tlo = 0,
+                      uint64_t thi = 0) {
     set_error("");
     if (!dfa || !d_result) { set_error("null dfa or result"); return PAREM_EINVAL; }
     if (n > 0 && !d_input) { set_error("null input"); return PAREM_EINVAL; }
@@ -171,6 +172,9 @@ static int match_impl(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, 
         find_bind(plan, P, reinterpret_cast<unsigned char*>(d_ws) + ((plan.ws + 255) & ~(size_t)255));
         P.fout = d_positions;
         P.fmax = d_positions ? max_positions : 0;
+        P.tout = d_trace;
+        P.tlo = tlo;
+        P.thi = thi;
         if (plan.kernel != kKernelTiny) P.fmend = nullptr;   // only the tiny kernel keeps dense maps
     }
     int rc2;
@@ -678,6 +682,22 @@ extern "C" int parem_find_async(const parem_dfa* dfa, const uint8_t* d_input, ui
                                 parem_result* d_result, void* stream) {
     return match_impl(dfa, d_input, n, 0, d_ws, ws_bytes, opts, nullptr, d_result, (cudaStream_t)stream, d_positions,
                       max_positions, true);
+}
+
+extern "C" int parem_trace_async(const parem_dfa* dfa, const uint8_t* d_input, uint64_t n, void* d_ws, size_t ws_bytes,
+                                 const parem_options* opts, uint64_t lo, uint64_t hi, uint32_t* d_states,
+                                 parem_result* d_result, void* stream) {
+    if (lo > hi || hi > n) {
+        set_error("trace window [%llu, %llu) outside the input (n = %llu)", (unsigned long long)lo,
+                  (unsigned long long)hi, (unsigned long long)n);
+        return PAREM_EINVAL;
+    }
+    if (hi > lo && !d_states) {
+        set_error("null trace buffer");
+        return PAREM_EINVAL;
+    }
+    return match_impl(dfa, d_input, n, 0, d_ws, ws_bytes, opts, nullptr, d_result, (cudaStream_t)stream, nullptr, 0, true,
+                      d_states, lo, hi);
 }
 
 extern "C" int parem_profile(int enable) {

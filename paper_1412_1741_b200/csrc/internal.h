@@ -86,6 +86,8 @@ struct MatchParams {
     void* maps;                // tiny: tile maps [grid][Qpad] u64; lanes: ends [p][Qpad] u32 + hits
     uint32_t* map_hits;        // lanes only
     // parem_find_async (NEXT-4; kernels_find.cu): null for a plain match
+    uint32_t* tout;            // parem_trace_async: visited states of the window [tlo, thi)
+    uint64_t tlo, thi;
     uint64_t* fout;            // match end offsets
     uint64_t fmax;             // capacity of fout
     uint32_t* fchunk_q;        // [p] entering state of chunk i

@@ -56,6 +56,9 @@ static_assert(sizeof(ConvChunk) == 64, "ConvChunk");
 // shrank to 32 states).
 constexpr uint32_t kMaxSurv = 32;
 constexpr uint32_t kWide = 0xFFFFFFFFu;
+// WsHeader::err bits of the converging path
+constexpr uint32_t kErrUnsound = 1u;   // a state entered a chunk that its candidate set does not hold: EINTERNAL
+constexpr uint32_t kErrWide = 4u;      // some chunk is wide (conv_wide_kernel has work)
 struct SurvRec {
     uint32_t n;
     uint32_t z[kMaxSurv];
@@ -1118,7 +1121,7 @@ __global__ void __launch_bounds__(kFollowThreads) conv_ends_kernel(const MatchPa
     EndSet& es = W.ends[t];
     if (W.info[t].D == kWide) {   // resolved by conv_wide_kernel from its entering set
         es.n = 0;
-        atomicOr(&P.hdr->err, 4u);
+        atomicOr(&P.hdr->err, kErrWide);
         return;
     }
     uint32_t n = 0;
@@ -1139,7 +1142,7 @@ __global__ void __launch_bounds__(kFollowThreads) conv_ends_kernel(const MatchPa
 // every other chunk stays on the parallel path.
 template <bool W32>
 __global__ void conv_wide_kernel(const MatchParams P) {
-    if (threadIdx.x >= 32 || !(P.hdr->err & 4u)) return;
+    if (threadIdx.x >= 32 || !(P.hdr->err & kErrWide)) return;
     const uint32_t lane = threadIdx.x;
     const ConvWs W = conv_ws(P);
     const DevDfa& d = P.d;
@@ -1225,7 +1228,7 @@ __global__ void __launch_bounds__(kFollowThreads) conv_map1_kernel(const MatchPa
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t A = d.A;
     unsigned long long rc = 0, steps = 0, lkm = 0;
-    if (t < P.p && !(P.hdr->err & 2u) && W.info[t].D != kWide && (t == 0 || W.ends[t - 1].n == 1)) {
+    if (t < P.p && W.info[t].D != kWide && (t == 0 || W.ends[t - 1].n == 1)) {
         const uint64_t b0 = conv_b(P, t), b1 = conv_b(P, t + 1);
         const ConvChunk& c = W.info[t];
         const SurvRec& s = W.surv[t];
@@ -1236,7 +1239,7 @@ __global__ void __launch_bounds__(kFollowThreads) conv_map1_kernel(const MatchPa
         uint32_t k = 0;
         while (k < s.n && s.z[k] != z) ++k;
         if (k == s.n) {
-            atomicOr(&P.hdr->err, 1u);   // speculation unsound: cannot happen
+            atomicOr(&P.hdr->err, kErrUnsound);   // speculation unsound: cannot happen
             k = 0;
         }
         W.maps[t].idx[0] = s.eidx[k];
@@ -1283,9 +1286,8 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_map_kernel(const MatchPar
     const ConvWs W = conv_ws(P);
     const uint8_t* in = P.in;
     const uint32_t A = d.A;
-    const bool skip = (P.hdr->err & 2u) != 0;   // wide chunks: the sequential fallback resolves
     unsigned long long routes = 0, steps = 0, lkw = 0;
-    for (uint64_t t = (uint64_t)blockIdx.x * kSetWarps + warp; t < P.p && !skip; t += (uint64_t)gridDim.x * kSetWarps) {
+    for (uint64_t t = (uint64_t)blockIdx.x * kSetWarps + warp; t < P.p; t += (uint64_t)gridDim.x * kSetWarps) {
         if (t == 0 || W.info[t].D == kWide) continue;   // wide: conv_wide_kernel's
         const uint32_t nin = W.ends[t - 1].n;
         if (nin <= 1) continue;   // conv_map1_kernel's
@@ -1316,7 +1318,7 @@ __global__ void __launch_bounds__(kSetWarps * 32) conv_map_kernel(const MatchPar
             uint32_t k = 0;
             while (k < s.n && s.z[k] != z) ++k;
             if (k == s.n) {
-                atomicOr(&P.hdr->err, 1u);   // speculation unsound: cannot happen
+                atomicOr(&P.hdr->err, kErrUnsound);   // speculation unsound: cannot happen
                 k = 0;
             }
             W.maps[t].idx[lane] = s.eidx[k];
@@ -1349,7 +1351,7 @@ __global__ void __launch_bounds__(kFollowThreads) conv_block_kernel(const MatchP
     const uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t nb = (P.p + kBlk - 1) / kBlk;
-    if (b >= nb || (P.hdr->err & 2u)) return;
+    if (b >= nb) return;
     const ConvWs W = conv_ws(P);
     const uint64_t c0 = b * kBlk, c1 = min(P.p, c0 + kBlk);
     const uint32_t nin = c0 == 0 ? 1u : W.ends[c0 - 1].n;
@@ -1363,7 +1365,7 @@ __global__ void __launch_bounds__(kFollowThreads) conv_super_kernel(const MatchP
     const uint64_t sb = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t nb = (P.p + kBlk - 1) / kBlk, ns = (nb + kBlk - 1) / kBlk;
-    if (sb >= ns || (P.hdr->err & 2u)) return;
+    if (sb >= ns) return;
     const ConvWs W = conv_ws(P);
     const uint64_t b0 = sb * kBlk, b1 = min(nb, b0 + kBlk);
     const uint64_t c0 = b0 * kBlk;
@@ -1377,7 +1379,7 @@ __global__ void __launch_bounds__(kFollowThreads) conv_super_kernel(const MatchP
 // E4b resolves the entering index of every block (thread per super-block).
 __global__ void conv_path_kernel(const MatchParams P) {
     const uint32_t lane = threadIdx.x & 31u;
-    if (threadIdx.x >= 32 || (P.hdr->err & 2u)) return;
+    if (threadIdx.x >= 32) return;
     const ConvWs W = conv_ws(P);
     const uint64_t nb = (P.p + kBlk - 1) / kBlk, ns = (nb + kBlk - 1) / kBlk;
     uint32_t e = 0;
@@ -1398,7 +1400,7 @@ __global__ void conv_path_kernel(const MatchParams P) {
 __global__ void __launch_bounds__(kFollowThreads) conv_blockin_kernel(const MatchParams P) {
     const uint64_t sb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t nb = (P.p + kBlk - 1) / kBlk, ns = (nb + kBlk - 1) / kBlk;
-    if (sb >= ns || (P.hdr->err & 2u)) return;
+    if (sb >= ns) return;
     const ConvWs W = conv_ws(P);
     uint32_t e = W.sin[sb];
     const uint64_t b0 = sb * kBlk, b1 = min(nb, b0 + kBlk);
@@ -1419,9 +1421,8 @@ __global__ void __launch_bounds__(kFollowThreads) conv_resolve_kernel(const Matc
     const ConvWs W = conv_ws(P);
     const uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t nb = (P.p + kBlk - 1) / kBlk;
-    const bool seq = (P.hdr->err & 2u) != 0;
     unsigned long long hits = 0;
-    if (b < nb && !seq) {
+    if (b < nb) {
         bool dead;
         const uint32_t q0 = start_state(P, &dead);
         uint32_t e = W.bin[b];
@@ -1450,7 +1451,7 @@ __global__ void __launch_bounds__(kFollowThreads) conv_resolve_kernel(const Matc
     const volatile WsHeader* h = P.hdr;
     // internal invariant violated: report instead of a wrong answer -- unless a byte was
     // outside the alphabet (ESYMBOL wins; such a boundary gets a placeholder candidate)
-    if ((h->err & 1u) && h->bad_inv == 0ull) {
+    if ((h->err & kErrUnsound) && h->bad_inv == 0ull) {
         parem_result r;
         memset(&r, 0, sizeof(r));
         r.final_state = PAREM_DEAD;

@@ -462,6 +462,39 @@ __global__ void __launch_bounds__(kFindThreads) find_emit_lanes_kernel(const Mat
     for (; a < b1; ++a) step(P.in[a], a);
 }
 
+// ---- route trace (parem_trace_async): the visited states of every chunk that meets the
+// window [tlo, thi), walked from the chunk's true entering state (Alg. 1's Rr of the route the
+// join selects).  One generic kernel for both table classes (global tables). ----
+__global__ void __launch_bounds__(kFindThreads) find_trace_kernel(const MatchParams P) {
+    const DevDfa& d = P.d;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= P.p) return;
+    const uint64_t b0 = find_b(P, t), b1 = find_b(P, t + 1);
+    if (b1 <= P.tlo || b0 >= P.thi) return;
+    const uint64_t end = min(b1, P.thi);
+    const uint32_t A = d.A, Qpad = d.Qpad;
+    const bool tiny = d.lanes_tab == nullptr;
+    uint32_t s = P.fchunk_q[t];
+    auto step = [&](uint32_t c, uint64_t k) {
+        c = c < A ? c : A - 1u;   // ESYMBOL inputs: any in-table column (the trace is unspecified)
+        if (tiny) s = __ldg(d.tab1 + s * A + c) & 0x7FFFu;
+        else if (d.lanes_u32) s = (__ldg(reinterpret_cast<const uint32_t*>(d.lanes_tab) + (size_t)c * Qpad + s) & ((Qpad - 1u) * 4u)) >> 2;
+        else s = (__ldg(reinterpret_cast<const uint16_t*>(d.lanes_tab) + (size_t)c * Qpad + s) & ((Qpad - 1u) * 2u)) >> 1;
+        if (k >= P.tlo) P.tout[k - P.tlo] = (d.has_sink && s == d.sink) ? PAREM_DEAD : s;
+    };
+    uint64_t a = b0;
+    for (; a < end && (((uintptr_t)(P.in + a)) & 15u); ++a) step(P.in[a], a);
+    for (; a + 16 <= end; a += 16) {
+        const uint4 x = ldg_v4_na(P.in + a);
+        const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k) step(__byte_perm(w4[q], 0u, 0x4440u | k), a + 4 * q + k);
+    }
+    for (; a < end; ++a) step(P.in[a], a);
+}
+
 unsigned nblk(uint64_t n, uint32_t per) { return (unsigned)((n + per - 1) / per); }
 
 }  // namespace
@@ -517,6 +550,16 @@ int launch_find(const Plan& plan, const MatchParams& P, cudaStream_t s) {
         find_lanes_seq_kernel<<<1, 32, 0, s>>>(P);
         prof_after("find_resolve", s);
     }   // converging path: q_i and h_i were written by conv_resolve
+    if (P.tout) {   // route trace instead of match positions
+        if (P.thi > P.tlo) find_trace_kernel<<<nblk(p, kFindThreads), kFindThreads, 0, s>>>(P);
+        prof_after("find_trace", s);
+        const cudaError_t te = cudaGetLastError();
+        if (te != cudaSuccess) {
+            set_error("trace kernel: %s", cudaGetErrorString(te));
+            return PAREM_ECUDA;
+        }
+        return PAREM_OK;
+    }
     find_scan_sums_kernel<<<(unsigned)nb, kScanBlock / 4, 0, s>>>(P);
     prof_after("find_scan_sums", s);
     find_scan_blocks_kernel<<<1, 32, 0, s>>>(P, nb);

@@ -621,3 +621,68 @@ def test_conv_invalid_byte_before_boundaries(parem, torch_mod):
         x[bad] = 250
         got = check(parem, torch_mod, c.table, c.start, c.accept, x, parem.options(chunk_len=L, kernel="conv"))
         assert got.status == parem.PAREM_ESYMBOL and got.bad_offset == bad[0]
+
+
+# ---------------------------------------------------------------- route trace (NEXT-4, Rr)
+def test_trace_paper_example_table2(parem, torch_mod):
+    """Table II's "Visited states": the routes the join selects are P0 from {0},
+    P1 from {1}, P2 from {7} and P3 from {0}; their concatenation is the trace."""
+    t = synth.kmp_dfa([0, 1, 2, 1, 4, 4, 3, 4], 5, np.uint32)
+    acc = np.zeros(9, dtype=bool)
+    acc[8] = True
+    x = np.array(["parel".index(ch) for ch in "plaraparallelapareparapl"], np.uint8)
+    want = [1, 0, 0, 0, 0, 1,  2, 3, 4, 5, 6, 7,  8, 0, 1, 2, 3, 0,  1, 2, 3, 4, 1, 0]   # P:177-185
+    with parem.Dfa(t, 0, acc) as d:
+        for opts in (parem.options(chunk_len=6, boundary="grid"), None):
+            r, st = d.trace(to_dev(torch_mod, x), opts=opts)
+            assert r.status == 0 and r.match_count == 1
+            assert st.cpu().tolist() == want
+        r, st = d.trace(to_dev(torch_mod, x), 5, 14, parem.options(chunk_len=6, boundary="grid"))
+        assert st.cpu().tolist() == want[5:14]
+        r, st = d.trace(to_dev(torch_mod, x), 7, 7)
+        assert st.numel() == 0 and r.match_count == 1
+        with pytest.raises(Exception):
+            d.trace(to_dev(torch_mod, x), 5, 25)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_trace_configs(parem, torch_mod, k):
+    """Every visited state of the CI-sized configs (tiny kernel, converging path) against the
+    oracle's prefix walks (oracle.states_at), whole input and an unaligned window."""
+    c = synth.config(k, n=(1 << 18) + 5)
+    x = c.make_input()
+    n = x.size
+    ref = oracle.states_at(c.table, c.start, x, np.arange(1, n + 1))
+    with parem.Dfa(c.table, c.start, c.accept) as d:
+        r, st = d.trace(to_dev(torch_mod, x, offset=3))
+        assert r.status == 0
+        assert np.array_equal(st.cpu().numpy().astype(np.uint32), ref)
+        lo, hi = 70001, 200003
+        for opts in (None, parem.options(chunk_len=777, boundary="grid")):
+            r, st = d.trace(to_dev(torch_mod, x), lo, hi, opts)
+            assert np.array_equal(st.cpu().numpy().astype(np.uint32), ref[lo:hi])
+
+
+def test_trace_lanes_and_dead(parem, torch_mod):
+    """The lanes kernel (partial table: sink state) and death: PAREM_DEAD from the dying symbol on."""
+    t = synth.partial_dfa(64, 6, 0.0005, 17, np.uint16)
+    acc = np.zeros(64, dtype=bool)
+    acc[::5] = True
+    x = np.random.default_rng(5).integers(0, 6, 50000).astype(np.uint8)
+    ref = oracle.walk(t, 0, acc, x)
+    with parem.Dfa(t, 0, acc) as d:
+        r, st = d.trace(to_dev(torch_mod, x), opts=parem.options(chunk_len=1000))
+    got = st.cpu().numpy().astype(np.uint32)
+    # replay the definition on the host (plain walk of the test's own table)
+    want = np.empty(x.size, np.uint32)
+    s, dead = 0, False
+    for i, cc in enumerate(x):
+        if not dead:
+            nx = int(t[s, cc])
+            if nx == 0xFFFF:
+                dead = True
+            else:
+                s = nx
+        want[i] = 0xFFFFFFFF if dead else s
+    assert np.array_equal(got, want)
+    assert (r.final_state == parem.PAREM_DEAD) == dead and r.match_count == ref.match_count

@@ -29,6 +29,8 @@ for seed in range(int(sys.argv[1]) if len(sys.argv) > 1 else 300):
     # the converging path's opt-in variants (read by the planner on every call)
     os.environ["PAREM_CONV_TMA"] = str(int(rng.random() < 0.3))
     os.environ["PAREM_CONV_REP"] = str(int(rng.choice([0, 0, 8, 16])))
+    os.environ["PAREM_CONV_HYB"] = str(int(rng.random() < 0.3))   # hybrid follow table (Q <= 1024, L2 tables)
+    os.environ["PAREM_CONV_CPT"] = str(int(rng.choice([1, 1, 2])))  # chunks per follow thread (interleaved walk)
     ref = oracle.walk(t, q0, acc, x)
     buf = torch.empty(n + 32, dtype=torch.uint8, device="cuda")
     off = int(rng.integers(0, 16))
