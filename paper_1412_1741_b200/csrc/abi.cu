@@ -236,26 +236,37 @@ bool batch_plan(const parem_dfa* dfa, uint64_t n, uint64_t count, const parem_op
     if (make_plan(dfa, n, opts, plan) != PAREM_OK || plan->kernel != kKernelTiny || !plan->tma) return false;
     const uint64_t rows = (uint64_t)kTinyThreads * kTinyRowsPerThread;   // chunks per CTA tile
     const int sms = dfa->num_sms > 0 ? dfa->num_sms : 148;
+    // Chunks per input cpi = n / L: whole CTA tiles (cpi a multiple of `rows`), or -- short
+    // inputs -- a whole number of warps with several inputs per tile (cpi = 64 .. rows / 2, a
+    // power of two), so that 1 MiB inputs still get 4 KiB chunks instead of 512 B ones.
+    // Cost: waves x (boxes per row + ~10 box-times of fixed cost per CTA wave; measured on
+    // 508 x 1 MiB: 512-byte chunks in 7 waves ran at 2.46 TB/s, 17 us of 31 us per wave fixed).
     uint64_t bestL = 0, best = ~0ull;
-    for (uint64_t L = 64; L <= 4096; L *= 2) {
+    const uint64_t warp_rows = 32ull * kTinyRowsPerThread;
+    for (uint64_t L = 64; L <= 16384; L *= 2) {
         if (opts && opts->chunk_len && opts->chunk_len != L) continue;
-        if (n % (rows * L)) continue;
-        const uint64_t ctas = count * (n / (rows * L));
+        if (n % L) continue;
+        const uint64_t c = n / L;
+        const bool whole = c % rows == 0;
+        const bool sub = c >= warp_rows && c < rows && rows % c == 0;
+        if (!whole && !sub) continue;
+        const uint64_t ctas = (count * c + rows - 1) / rows;
         const uint64_t waves = (ctas + sms - 1) / sms;
-        const uint64_t cost = waves * (L / 64 + 2);   // ~2 box-times of fixed cost per CTA
+        const uint64_t cost = waves * (L / 64 + 10);
         if (cost < best) { best = cost; bestL = L; }
     }
     if (!bestL) return false;
     *cpi = n / bestL;
-    const uint64_t ctas = count * (n / (rows * bestL));
+    const uint64_t ctas = (count * *cpi + rows - 1) / rows;
     if (ctas > 0x7FFFFFFFull) return false;
+    const uint64_t spt = *cpi < rows ? rows / *cpi : 1;   // inputs (maps) per CTA tile
     plan->L = bestL;
     plan->p = count * *cpi;
     plan->grid = ctas;
     plan->policy = PAREM_BOUNDARY_GRID;
     plan->win = 0;
     plan->off_maps = 256 + ((count * 32 + 255) & ~255ull);
-    plan->ws = ((plan->off_maps + ctas * dfa->dev.Qpad * 8) + 255) & ~(size_t)255;
+    plan->ws = ((plan->off_maps + ctas * spt * dfa->dev.Qpad * 8) + 255) & ~(size_t)255;
     return true;
 }
 }  // namespace

@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
         const unsigned long long ss = warp_sum((ca.live ? (unsigned long long)ca.rc * (ca.b1 - ca.b0) : 0ull) +
                                                (cb.live ? (unsigned long long)cb.rc * (cb.b1 - cb.b0) : 0ull));
         if (lane == 0 && rs) {
-            // a warp's 64 chunks never span two batch inputs (inputs are whole CTA tiles)
+            // a warp's 64 chunks never span two batch inputs (inputs are whole numbers of warps)
             unsigned long long* st = P.cpi ? P.bstats + 4 * (row0 / P.cpi) + 1 : &P.hdr->routes;
             atomicAdd(st, (unsigned long long)rs);
             atomicAdd(st + 1, ss);
@@ -495,17 +495,22 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
     }
     __syncthreads();
 
+    // Tile maps.  A batch of SHORT inputs (cpi < kRows chunks each, a whole number of warps)
+    // packs spt = kRows / cpi inputs into one CTA tile: warp j composes the warp maps of
+    // sub-tile j only, so no map ever spans two inputs and chunks can stay long.
     unsigned long long* tiles = reinterpret_cast<unsigned long long*>(P.maps);
-    if (warp == 0) {
+    const uint32_t spt = (P.cpi && P.cpi < kRows) ? kRows / (uint32_t)P.cpi : 1u;
+    if (warp < spt) {
+        const uint32_t wps = kWarps / spt;
         uint32_t ce = lane < Qpad ? lane : 0;
         unsigned long long ch = 0;
-        for (uint32_t w = 0; w < kWarps; ++w) {
+        for (uint32_t w = warp * wps; w < (warp + 1) * wps; ++w) {
             const uint32_t row = w * Qpad + ce;
             const uint32_t ne = wend[row];
             ch += whits[row];
             ce = ne;
         }
-        if (lane < Qpad) tiles[(uint64_t)blockIdx.x * Qpad + lane] = (ch << 8) | ce;
+        if (lane < Qpad) tiles[((uint64_t)blockIdx.x * spt + warp) * Qpad + lane] = (ch << 8) | ce;
         __threadfence();
     }
     __syncthreads();
@@ -518,8 +523,8 @@ __global__ void __launch_bounds__(kT, 1) tiny_kernel(const MatchParams P, const 
     __threadfence();
 
     if (P.cpi) {   // batch: one fold per input, warp w takes inputs w, w + 16, ...
-        const uint32_t tpi = (uint32_t)(P.cpi / kRows);   // CTA tiles per input
-        const uint32_t nin = gridDim.x / tpi;
+        const uint32_t tpi = P.cpi >= kRows ? (uint32_t)(P.cpi / kRows) : 1u;   // maps per input
+        const uint32_t nin = (uint32_t)(P.p / P.cpi);
         for (uint32_t b = warp; b < nin; b += kWarps) {
             uint32_t ce = lane < Qpad ? lane : 0;
             unsigned long long ch = 0;

@@ -64,6 +64,23 @@ def test_batch_single_launch_matches_oracle(parem, torch_mod, k, count, n):
     expect_all(cfg, X, got)
 
 
+@pytest.mark.parametrize("k,count,n,L", [(1, 5, 1 << 16, 1024), (1, 7, 1 << 16, 256), (2, 9, 1 << 17, 256),
+                                         (2, 3, 1 << 15, 512), (1, 33, 1 << 20, 4096), (2, 4, 1 << 20, 1024),
+                                         (2, 2, 1 << 21, 64)])
+def test_batch_short_inputs_share_tiles(parem, torch_mod, k, count, n, L):
+    """Forced chunk lengths: inputs of fewer chunks than a CTA tile (cpi = n / L = 64 .. 512)
+    are packed several per tile (one sub-tile map each), a partly filled last tile included;
+    cpi >= 1024 keeps whole tiles per input.  Stats are those of a single GRID match."""
+    cfg = synth.config(k)
+    X = batch_inputs(cfg, count, n, 21)
+    got = run_batch(parem, torch_mod, cfg, X, parem.options(ws_clean=True, chunk_len=L), reuse=2)
+    expect_all(cfg, X, got)
+    assert all(g.num_chunks == n // L for g in got)
+    b = oracle.grid_boundaries(n, L)
+    for i in (0, count - 1):
+        assert (got[i].routes, got[i].route_steps) == oracle.route_stats(cfg.table, X[i], b)
+
+
 @pytest.mark.parametrize("n", [100003, 1000, 1, 65536 + 16])
 def test_batch_fallback_sizes(parem, torch_mod, n):
     # not whole tiles: the inputs are matched one after another (same results)
