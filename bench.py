@@ -310,15 +310,24 @@ class Micro:
         if key in self.cache:
             return self.cache[key]
         rng = np.random.default_rng(0)
-        tab = torch.from_numpy(rng.integers(0, 1 << 16, entries).astype(np.uint16)).to(self.dev)
-        lk = C.c_uint64()
-        ms = self.P.lib().parem_bench_gather(where, C.c_void_p(tab.data_ptr()), entries, 256,
-                                             C.c_void_p(self._sink().data_ptr()), C.byref(lk), 3,
-                                             C.c_void_p(self.stream.cuda_stream))
-        torch.cuda.synchronize()
-        v = float(f"{lk.value / (ms * 1e-3):.4g}") if ms > 0 else None
-        self.cache[key] = v
-        return v
+        host = rng.integers(0, 1 << 16, entries).astype(np.uint16)
+        # the best of three table allocations: the L2 gather rate moves ~10 % with where the
+        # table lands in the two dies' L2 slices (312-361e9/s seen for 512 KiB), and a peak
+        # is the best the level sustains
+        best, keep = None, []
+        for _ in range(3 if where == 1 else 1):
+            tab = torch.from_numpy(host).to(self.dev)
+            keep.append(tab)
+            lk = C.c_uint64()
+            ms = self.P.lib().parem_bench_gather(where, C.c_void_p(tab.data_ptr()), entries, 256,
+                                                 C.c_void_p(self._sink().data_ptr()), C.byref(lk), 3,
+                                                 C.c_void_p(self.stream.cuda_stream))
+            torch.cuda.synchronize()
+            if ms > 0:
+                v = float(f"{lk.value / (ms * 1e-3):.4g}")
+                best = v if best is None else max(best, v)
+        self.cache[key] = best
+        return best
 
     def summary(self):
         out = {}
