@@ -631,28 +631,71 @@ struct Follow {
     uint32_t e[CPT][kDMax], h[CPT][kDMax];
     uint32_t bad, A, wmask, K, K7F;   // K = (256 - A) per byte, K7F = K & 0x7F7F7F7F
     bool check;
-    // Per-lane merging (NEXT-2 (ii)): Dl = routes of chunk j still walked.  Once all routes
-    // of a chunk are in one state the lane walks route 0 only (Dl = 1) and keeps, in h[j][k],
-    // route k's hit OFFSET against route 0 at the meeting point; the predicated-off lookups
-    // issue no L1TEX wavefronts, which is what bounds the walk (the slowest lane of the
-    // warp no longer makes every lane pay kDMax lookups per byte).  finish() rebuilds.
-    uint32_t Dl[CPT];
-    uint32_t mv[CPT];   // 16-byte vectors walked with all D routes (stats: hdr->lookups)
+    // Per-lane merging (NEXT-2 (ii)): slots [0, Dl) of chunk j hold the routes still walked.
+    // Every check merges routes that are in the same state PAIRWISE: the higher slot k is
+    // retired into the lower slot r -- the last live slot moves into slot k, and the freed
+    // slot Dl - 1 keeps the record of the retired route (survivor id, its carrier's survivor
+    // id, its hit offset against the carrier at the meeting point).  The hot loop's
+    // predicate stays "k < Dl"; predicated-off lookups issue no L1TEX wavefronts, which is
+    // what bounds the walk (the slowest lane of the warp no longer makes every lane pay
+    // kDMax lookups per byte).  sid = slot -> survivor id (2 bits each).  finish() rebuilds
+    // every survivor's (end, hits) in survivor order.
+    uint32_t Dl[CPT], sid[CPT];
+    uint32_t mv[CPT];   // sum over retired routes of the 16-byte vectors they walked (stats)
 
     __device__ __forceinline__ Follow(const TT& t) : T(t) {}
 
+    __device__ __forceinline__ void begin(int j) {
+        Dl[j] = D[j];
+        sid[j] = 0xE4u;   // slot k holds survivor k
+        mv[j] = 0;
+    }
+    // retire slot K into slot R (R < K < Dl), written for compile-time K, R, LAST = Dl - 1
+    template <int R, int K, int LAST>
+    __device__ __forceinline__ void retire(int j) {
+        const uint32_t off = h[j][K] - h[j][R];   // u32 wrap-around is exact
+        const uint32_t idk = (sid[j] >> (2 * K)) & 3u, idr = (sid[j] >> (2 * R)) & 3u, idl = (sid[j] >> (2 * LAST)) & 3u;
+        if (K != LAST) {
+            e[j][K] = e[j][LAST];
+            h[j][K] = h[j][LAST];
+        }
+        e[j][LAST] = idr;   // record of the retired route, kept in the freed slot
+        h[j][LAST] = off;
+        uint32_t sd = sid[j] & ~((3u << (2 * K)) | (3u << (2 * LAST)));
+        sd |= idl << (2 * K);      // (K == LAST: overwritten by the next line)
+        sd = (sd & ~(3u << (2 * LAST))) | (idk << (2 * LAST));
+        sid[j] = sd;
+    }
     // true when chunk j walks one route (now or already)
     __device__ __forceinline__ bool lane_merge(int j, uint32_t vdone) {
-        if (Dl[j] > 1u) {
-            bool same = true;
+        static_assert(kDMax == 4, "lane_merge / finish are written out for 4 routes");
+        // at most Dl - 1 retirements; each pass retires the first equal pair it finds
 #pragma unroll
-            for (int k = 1; k < (int)kDMax; ++k) same &= (uint32_t)k >= Dl[j] || T.state(e[j][k]) == T.state(e[j][0]);
-            if (same) {
-#pragma unroll
-                for (int k = 1; k < (int)kDMax; ++k) h[j][k] -= h[j][0];   // u32 wrap-around is exact
-                Dl[j] = 1u;
-                mv[j] = vdone;
+        for (int pass = 0; pass < 3; ++pass) {
+            const uint32_t n = Dl[j];
+            if (n <= 1u) break;
+            const uint32_t s0 = T.state(e[j][0]), s1 = T.state(e[j][1]), s2 = T.state(e[j][2]), s3 = T.state(e[j][3]);
+            bool did = true;
+            if (n == 2u) {
+                if (s1 == s0) retire<0, 1, 1>(j);
+                else did = false;
+            } else if (n == 3u) {
+                if (s1 == s0) retire<0, 1, 2>(j);
+                else if (s2 == s0) retire<0, 2, 2>(j);
+                else if (s2 == s1) retire<1, 2, 2>(j);
+                else did = false;
+            } else {
+                if (s1 == s0) retire<0, 1, 3>(j);
+                else if (s2 == s0) retire<0, 2, 3>(j);
+                else if (s3 == s0) retire<0, 3, 3>(j);
+                else if (s2 == s1) retire<1, 2, 3>(j);
+                else if (s3 == s1) retire<1, 3, 3>(j);
+                else if (s3 == s2) retire<2, 3, 3>(j);
+                else did = false;
             }
+            if (!did) break;
+            Dl[j] = n - 1u;
+            mv[j] += vdone;
         }
         return Dl[j] <= 1u;
     }
@@ -694,23 +737,51 @@ struct Follow {
         }
     }
 
-    // lookups of chunk j over `bytes` bytes, `head` of them before the 16-byte vectors
+    // lookups of chunk j over `bytes` bytes, `head` of them before the 16-byte vectors:
+    // routes still live walked every byte, a retired route walked up to its meeting point
     __device__ __forceinline__ unsigned long long chunk_lookups(int j, uint64_t bytes, uint64_t head) const {
         if (D[j] <= 1u) return bytes;
-        const uint64_t wide = mv[j] == 0xFFFFFFFFu ? bytes : min(bytes, head + (uint64_t)16 * mv[j]);
-        return bytes + (uint64_t)(D[j] - 1u) * wide;
+        const uint64_t nret = D[j] - Dl[j];
+        return bytes * Dl[j] + min(bytes * nret, head * nret + (uint64_t)16 * mv[j]);
     }
+    // rebuild every survivor's (entry, hits): live slots first, then the retired records from
+    // the LAST retirement to the first (slots Dl .. D - 1 ascending), so that a carrier --
+    // live, or retired later than its rider -- is final before the rider reads it
     __device__ __forceinline__ void finish() {
 #pragma unroll
-        for (int j = 0; j < CPT; ++j)
-            if (D[j] > 1u && Dl[j] == 1u) {
+        for (int j = 0; j < CPT; ++j) {
+            if (D[j] <= 1u || Dl[j] == D[j]) continue;
+            uint32_t fe[kDMax], fh[kDMax];
 #pragma unroll
-                for (int k = 1; k < (int)kDMax; ++k) {
-                    h[j][k] += h[j][0];
-                    e[j][k] = e[j][0];
+            for (int k = 0; k < (int)kDMax; ++k) fe[k] = fh[k] = 0;
+#pragma unroll
+            for (int sl = 0; sl < (int)kDMax; ++sl) {
+                if ((uint32_t)sl >= D[j]) continue;
+                const uint32_t id = (sid[j] >> (2 * sl)) & 3u;
+                uint32_t ve, vh;
+                if ((uint32_t)sl < Dl[j]) {
+                    ve = e[j][sl];
+                    vh = h[j][sl];
+                } else {
+                    const uint32_t c = e[j][sl] & 3u;   // carrier's survivor id
+                    ve = c == 0u ? fe[0] : c == 1u ? fe[1] : c == 2u ? fe[2] : fe[3];
+                    vh = (c == 0u ? fh[0] : c == 1u ? fh[1] : c == 2u ? fh[2] : fh[3]) + h[j][sl];
                 }
-                Dl[j] = D[j];
+#pragma unroll
+                for (int k = 0; k < (int)kDMax; ++k)
+                    if (id == (uint32_t)k) {
+                        fe[k] = ve;
+                        fh[k] = vh;
+                    }
             }
+#pragma unroll
+            for (int k = 0; k < (int)kDMax; ++k) {
+                e[j][k] = fe[k];
+                h[j][k] = fh[k];
+            }
+            Dl[j] = D[j];
+            sid[j] = 0xE4u;
+        }
     }
 
     template <int K>
@@ -855,8 +926,7 @@ __global__ void __launch_bounds__(kFollowThreads, 1) conv_follow_kernel(const Ma
         b1[j] = live ? conv_b(P, t[j] + 1) : b0;
         const uint32_t D0 = live ? info->D : 0u;
         F.D[j] = D0 == kWide ? 0u : D0;   // follow only handed-over chunks
-        F.Dl[j] = F.D[j];
-        F.mv[j] = 0xFFFFFFFFu;
+        F.begin(j);
         act[j] = F.D[j] != 0;
         a[j] = act[j] ? b0 + info->m : b1[j];
 #pragma unroll
@@ -969,8 +1039,7 @@ __global__ void __launch_bounds__(kFThreads) conv_follow_tma_kernel(const MatchP
     const uint64_t b0 = conv_b(P, t), b1 = live ? conv_b(P, t + 1) : b0;
     const uint32_t D0 = live ? info->D : 0u;
     F.D[0] = D0 == kWide ? 0u : D0;   // follow only handed-over chunks
-    F.Dl[0] = F.D[0];
-    F.mv[0] = 0xFFFFFFFFu;
+    F.begin(0);
     const bool act = F.D[0] != 0;
     const uint32_t m = act ? info->m : 0u;
 #pragma unroll
