@@ -311,9 +311,10 @@ class Micro:
             return self.cache[key]
         rng = np.random.default_rng(0)
         host = rng.integers(0, 1 << 16, entries).astype(np.uint16)
-        # the best of three table allocations: the L2 gather rate moves ~10 % with where the
-        # table lands in the two dies' L2 slices (312-361e9/s seen for 512 KiB), and a peak
-        # is the best the level sustains
+        # the best of three table allocations: the L2 gather rate differed ~10 % between runs
+        # (312-361e9/s for 512 KiB; within one process twelve allocations agree to 0.2 %,
+        # tools/placement_probe.py, so it is the box, not the placement), and a peak is the
+        # best the level sustains
         best, keep = None, []
         for _ in range(3 if where == 1 else 1):
             tab = torch.from_numpy(host).to(self.dev)

@@ -303,6 +303,24 @@ typedef struct parem_regex_info {
 int parem_regex_compile(const char* pattern, const char* alphabet, uint32_t flags, uint32_t max_states,
                         uint32_t* table, uint8_t* accept_bitmap, parem_regex_info* info);
 
+/* ---- transition-table text I/O ("the PaREM creates a log file with the
+ * transition table"; format S:184-188).  Host only.  UTF-8 / LF text:
+ *     symbols<TAB>s1<TAB>s2...        one character per symbol (\xHH for a byte that is not a
+ *                                     printable ASCII character other than backslash)
+ *     start<TAB><id>
+ *     finals[<TAB><id>...]            zero or more ids
+ *     <state-id><TAB><dest or ->...   one row per state in id order, '-' = DEAD
+ * parem_table_write_text: row-major uint32 table (PAREM_DEAD = missing), LSB-first accept bitmap,
+ * alphabet_size symbol bytes; *needed = bytes of text (no NUL); out == NULL is a size query;
+ * ENOMEM if cap < *needed.  parem_table_read_text: the inverse (read(write(d)) == d exactly);
+ * table / accept_bitmap == NULL is a size query (info->num_states, alphabet_size, start_state,
+ * alphabet); EINVAL on malformed text with "line N: reason" in parem_last_error(); ENOMEM if
+ * the table has more than max_states states. */
+int parem_table_write_text(uint32_t num_states, uint32_t alphabet_size, const uint32_t* table, uint32_t start_state,
+                           const uint8_t* accept_bitmap, const char* alphabet, char* out, size_t cap, size_t* needed);
+int parem_table_read_text(const char* text, size_t len, uint32_t max_states, uint32_t* table, uint8_t* accept_bitmap,
+                          parem_regex_info* info);
+
 /* ---- per-kernel timing (bench.py; off by default) ----
  * parem_profile(1) clears the record and makes every later match issued by this host
  * thread record CUDA events on its stream around each kernel it launches (not while the

@@ -21,7 +21,7 @@ from . import _abi
 from ._abi import (BOUNDARY_AUTO, BOUNDARY_GRID, BOUNDARY_SNAP, CANDIDATES_ENUM, CANDIDATES_PAREM, KERNEL_AUTO, KERNEL_CONV, KERNEL_LANES,
                    KERNEL_TINY, PAREM_DEAD, PAREM_EINVAL, PAREM_ESYMBOL, PAREM_OK)
 
-__all__ = ["Dfa", "MatchResult", "ParemError", "Regex", "compile_regex", "options", "profile", "profile_read", "PAREM_DEAD", "PAREM_OK",
+__all__ = ["Dfa", "MatchResult", "ParemError", "Regex", "compile_regex", "table_to_text", "table_from_text", "options", "profile", "profile_read", "PAREM_DEAD", "PAREM_OK",
            "PAREM_ESYMBOL", "PAREM_EINVAL", "lib", "SEGMAP_DTYPE", "fold_segment_maps", "exchange_and_fold", "shard_match"]
 
 
@@ -91,6 +91,47 @@ class Regex(NamedTuple):
         return ids
 
 
+def table_to_text(table, start: int, accept, alphabet: bytes) -> str:
+    """parem_table_write_text: the transition-table log file (format S:184-188).
+    ``table`` uint16/uint32 [Q, A] with DEAD = all-ones, ``accept`` bool [Q]."""
+    L = lib()
+    t = np.ascontiguousarray(table)
+    Q, A = t.shape
+    t32 = np.where(t == np.iinfo(t.dtype).max, np.uint32(0xFFFFFFFF), t.astype(np.uint32)).astype(np.uint32)
+    t32 = np.ascontiguousarray(t32)
+    bm = np.packbits(np.asarray(accept, dtype=bool), bitorder="little")
+    alp = bytes(alphabet)
+    if len(alp) != A:
+        raise ValueError("alphabet must name every symbol column")
+    need = C.c_size_t(0)
+    st = L.parem_table_write_text(Q, A, t32.ctypes.data, int(start), bm.ctypes.data, alp, None, 0, C.byref(need))
+    if st != PAREM_OK:
+        _err(L, st)
+    buf = C.create_string_buffer(need.value)
+    st = L.parem_table_write_text(Q, A, t32.ctypes.data, int(start), bm.ctypes.data, alp, buf, need.value, C.byref(need))
+    if st != PAREM_OK:
+        _err(L, st)
+    return buf.raw[: need.value].decode("latin-1")
+
+
+def table_from_text(text: str | bytes) -> Regex:
+    """parem_table_read_text: the inverse of table_to_text (uint32 table, PAREM_DEAD = missing)."""
+    L = lib()
+    raw = text.encode("latin-1") if isinstance(text, str) else bytes(text)
+    info = _abi.parem_regex_info()
+    st = L.parem_table_read_text(raw, len(raw), 0, None, None, C.byref(info))
+    if st != PAREM_OK:
+        _err(L, st)
+    Q, A = info.num_states, info.alphabet_size
+    tab = np.zeros((Q, A), dtype=np.uint32)
+    bm = np.zeros((Q + 7) // 8, dtype=np.uint8)
+    st = L.parem_table_read_text(raw, len(raw), Q, tab.ctypes.data, bm.ctypes.data, C.byref(info))
+    if st != PAREM_OK:
+        _err(L, st)
+    acc = np.unpackbits(bm, bitorder="little")[:Q].astype(bool)
+    return Regex(tab, int(info.start_state), acc, C.string_at(C.addressof(info) + _abi.parem_regex_info.alphabet.offset, A))
+
+
 def compile_regex(pattern: str | bytes, alphabet: str | bytes | None = None, search: bool = False,
                   max_states: int = 1 << 16) -> Regex:
     """parem_regex_compile: the paper's RE language (Table III) -> minimal DFA (NEXT-3).
@@ -110,7 +151,7 @@ def compile_regex(pattern: str | bytes, alphabet: str | bytes | None = None, sea
     if st != PAREM_OK:
         _err(L, st)
     acc = np.unpackbits(bm, bitorder="little")[:Q].astype(bool)
-    return Regex(tab, int(info.start_state), acc, bytes(info.alphabet[:A]))
+    return Regex(tab, int(info.start_state), acc, C.string_at(C.addressof(info) + _abi.parem_regex_info.alphabet.offset, A))
 
 
 def profile(enable: bool = True) -> None:

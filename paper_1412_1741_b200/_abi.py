@@ -61,7 +61,7 @@ EXPORTS = [
     "parem_dfa_create", "parem_dfa_destroy", "parem_workspace_bytes", "parem_match_async",
     "parem_match_continue_async", "parem_match", "parem_match_host", "parem_dfa_get_info", "parem_plan",
     "parem_last_error", "parem_version", "parem_bench_read_stream", "parem_bench_gather", "parem_profile",
-    "parem_profile_read", "parem_regex_compile", "parem_find_async", "parem_find_workspace_bytes", "parem_trace_async",
+    "parem_profile_read", "parem_regex_compile", "parem_table_write_text", "parem_table_read_text", "parem_find_async", "parem_find_workspace_bytes", "parem_trace_async",
     "parem_batch_workspace_bytes", "parem_match_batch_async", "parem_segment_map", "parem_fold_segment_maps",
 ]
 
@@ -109,6 +109,10 @@ def load(path: str = SO_PATH):
     L.parem_trace_async.argtypes = [vp, vp, u64, vp, sz, O, u64, u64, vp, vp, vp]
     L.parem_regex_compile.restype = i32
     L.parem_regex_compile.argtypes = [C.c_char_p, C.c_char_p, u32, u32, vp, vp, C.POINTER(parem_regex_info)]
+    L.parem_table_write_text.restype = i32
+    L.parem_table_write_text.argtypes = [u32, u32, vp, u32, vp, C.c_char_p, vp, sz, C.POINTER(sz)]
+    L.parem_table_read_text.restype = i32
+    L.parem_table_read_text.argtypes = [C.c_char_p, sz, u32, vp, vp, C.POINTER(parem_regex_info)]
     L.parem_profile.restype = i32
     L.parem_profile.argtypes = [i32]
     L.parem_profile_read.restype = i32

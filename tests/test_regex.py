@@ -131,3 +131,60 @@ def test_regex_on_gpu(P, cuda_device, pat, alpha):
     with P.Dfa(r.table, r.start, r.accept) as d:
         got = d.match(torch.from_numpy(x).to("cuda"))
     assert (got.final_state, got.accepted, got.match_count) == (ref.final_state, ref.accepted, ref.match_count)
+
+
+# ---------------------------------------------------------------- transition-table text I/O
+def test_table_text_table_I_layout(P):
+    """Table I as the log file of P:314 in SPEC's layout: header
+    `symbols p a r e l`, `start 0`, `finals 8`, nine rows; the text reads back exactly."""
+    r = P.compile_regex("parallel", "parel", search=True)
+    txt = P.table_to_text(r.table, r.start, r.accept, r.alphabet)
+    lines = txt.split("\n")
+    assert lines[0] == "symbols\tp\ta\tr\te\tl" and lines[1] == "start\t0" and lines[2] == "finals\t8"
+    assert len(lines) == 3 + 9 + 1 and lines[-1] == ""
+    assert lines[3 + 5] == "5\t1\t0\t0\t0\t6" and lines[3 + 7] == "7\t1\t0\t0\t0\t8"   # delta(5,l)=6, delta(7,l)=8
+    back = P.table_from_text(txt)
+    assert back.table.tolist() == r.table.tolist() and back.start == r.start
+    assert back.accept.tolist() == r.accept.tolist() and back.alphabet == r.alphabet
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_table_text_round_trip_random(P, seed):
+    """Round trip is the identity: random partial DFAs (DEAD entries as '-'), any
+    alphabet bytes (escaped when not printable), zero or many finals, u16 and u32 tables."""
+    rng = np.random.default_rng(seed)
+    Q, A = int(rng.integers(1, 60)), int(rng.integers(1, 40))
+    dt = np.uint16 if seed % 2 else np.uint32
+    t = synth.partial_dfa(Q, A, 0.3, seed, dt)
+    acc = rng.random(Q) < (0.0 if seed % 5 == 0 else 0.4)
+    alphabet = bytes(rng.permutation(256)[:A].astype(np.uint8))
+    start = int(rng.integers(0, Q))
+    txt = P.table_to_text(t, start, acc, alphabet)
+    back = P.table_from_text(txt)
+    want = np.where(t == np.iinfo(dt).max, 0xFFFFFFFF, t.astype(np.int64))
+    assert back.table.astype(np.int64).tolist() == want.tolist()
+    assert (back.start, back.accept.tolist(), back.alphabet) == (start, acc.tolist(), alphabet)
+    assert P.table_to_text(back.table, back.start, back.accept, back.alphabet) == txt
+
+
+@pytest.mark.parametrize("text,line", [
+    ("", 1), ("symbol\ta\nstart\t0\nfinals\n0\t0\n", 1), ("symbols\ta\ta\nstart\t0\nfinals\n0\t0\t0\n", 1),
+    ("symbols\ta\nstar\t0\nfinals\n0\t0\n", 2), ("symbols\ta\nstart\t5\nfinals\n0\t0\n", 2),
+    ("symbols\ta\nstart\t0\nfinals\t3\n0\t0\n", 3), ("symbols\ta\nstart\t0\nfinals\n1\t0\n", 4),
+    ("symbols\ta\tb\nstart\t0\nfinals\n0\t0\n", 4), ("symbols\ta\nstart\t0\nfinals\n0\t0\n1\t7\n", 5),
+    ("symbols\ta\nstart\t0\nfinals\n0\tx\n", 4), ("symbols\ta\nstart\t0\nfinals\n", 4),
+])
+def test_table_text_parse_errors_name_the_line(P, text, line):
+    with pytest.raises(P.ParemError) as ei:
+        P.table_from_text(text)
+    assert f"line {line}:" in str(ei.value), str(ei.value)
+
+
+def test_table_text_loaded_table_matches_like_the_original(P):
+    """A table written and read back drives the oracle to the same result (the pipeline of
+    S:437 without the GPU): Table I on the paper's worked input, count 1."""
+    r = P.compile_regex("parallel", "parel", search=True)
+    back = P.table_from_text(P.table_to_text(r.table, r.start, r.accept, r.alphabet))
+    x = back.encode(b"plaraparallelapareparapl")
+    ref = oracle.walk(back.table, back.start, back.accept, x)
+    assert (ref.final_state, ref.match_count) == (0, 1)
