@@ -159,11 +159,11 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
 
     if (kernel == kKernelConv) {
         // K2 follows one dependent chain per chunk: the chunk count is the number of
-        // lookups in flight (~1024 per SM: 512-thread CTAs, two per SM); the set walk's cost
-        // grows with the chunk count, and chunks stay long against the walk's head (~conv_t4
-        // symbols).  The follow streams its rows through TMA boxes of 64 bytes, so planner
-        // row lengths are whole boxes (and not multiples of 256 B: TMA row streams at such
-        // strides are slower, profiles/r01_stride_probe.txt).
+        // lookups in flight (one follow CTA per SM, one wave); the set walk's cost grows with
+        // the chunk count, and chunks stay long against the walk's head (~conv_t4 symbols).
+        // With the opt-in TMA-staged follow the rows are whole 64-byte boxes (and not
+        // multiples of 256 B: TMA row streams at such strides are slower,
+        // profiles/r01_stride_probe.txt).
         // Follow input: each thread streams its row with 16-byte loads that do not allocate
         // in L1 (an L2-resident table keeps the whole L1: carveout 0).  The TMA-staged
         // follow (conv_tma) is faster per byte on shared-memory tables but needs ~1024
