@@ -167,6 +167,7 @@ void find_bind(const Plan& plan, MatchParams& P, unsigned char* extra);
 size_t conv_ws_total(uint64_t p);
 size_t conv_rep_smem(const DevDfa& d, uint32_t R);        // 0 if the layout does not apply
 bool conv_hybrid_applies(const DevDfa& d);
+bool conv_byte_table_applies(const DevDfa& d);
 size_t conv_follow_tma_smem(size_t table_bytes);
 size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap, uint32_t warps);
 int launch_trivial(const MatchParams& P, cudaStream_t s);

@@ -138,7 +138,7 @@ __host__ __device__ __forceinline__ size_t tab_bytes(const DevDfa& d) {
 template <bool SMEM, bool W32>
 struct Tab {
     static constexpr uint32_t ES = W32 ? 4 : 2, ACC = W32 ? 31 : 15;
-    static constexpr bool kSmem = SMEM, kW32 = W32, kRep = false, kHyb = false;
+    static constexpr bool kSmem = SMEM, kW32 = W32, kRep = false, kHyb = false, kByte = false;
     const unsigned char* g;
     uint32_t cbase, COL, SMASK, CMASK;
 
@@ -209,7 +209,7 @@ __host__ __device__ __forceinline__ uint32_t rep_col_bytes(uint32_t Qpad, uint32
 template <int R>
 struct TabR {
     static constexpr uint32_t ES = 2;
-    static constexpr bool kSmem = true, kW32 = false, kRep = true, kHyb = false;
+    static constexpr bool kSmem = true, kW32 = false, kRep = true, kHyb = false, kByte = false;
     static constexpr int kR = R;
     uint32_t tbase, COL, FMASK, AM1, k;
 
@@ -265,6 +265,90 @@ __host__ __device__ __forceinline__ size_t rep_smem_bytes(const DevDfa& d, uint3
     return col > (1u << 15) ? 0 : (size_t)d.A * col + col;   // + alignment slack
 }
 
+// Byte-entry replicated table for the follow walk of DFAs with <= 256 states: sixteen copies of
+// a u8 table in shared memory, copy k = lane mod 16 in banks {2k, 2k+1} (eight states per
+// 128-byte row and copy), so only the two lanes that share a copy can conflict: 2 wavefronts
+// per lookup instead of the ~3.6 of 32 random lanes in one plain table -- what bounds the cfg3
+// follow (profiles/r02_ncu_full_cfg3_conv_follow.json).  With one byte per entry the 16 copies
+// of a 256 x 26 table take 104 KB (u16 entries: 208 KB, which starves the input streams'
+// L1).  A byte holds the state only, so states are renumbered inside the kernel -- accepting
+// states last -- and the accept flag is the comparison code >= Qpad - |F|.
+struct TabB {
+    static constexpr bool kSmem = true, kW32 = false, kRep = false, kHyb = false, kByte = true;
+    static constexpr uint32_t kBudget = 112u * 1024u;
+    uint32_t tbase, COL, AM1, k8, hitK, lgQ, cof, sof;
+
+    __host__ __device__ static uint32_t col_bytes(const DevDfa& d) { return d.Qpad * 16u; }
+    __host__ __device__ static bool applies(const DevDfa& d) {
+        return d.Qpad <= 256u && !d.has_sink && (size_t)d.A * col_bytes(d) <= kBudget;
+    }
+    __host__ __device__ static size_t bytes(const DevDfa& d) {
+        return (size_t)d.A * col_bytes(d) + col_bytes(d) + 512u;   // + alignment slack + the two code maps
+    }
+    __device__ __forceinline__ void init(const DevDfa& d, unsigned char* sm) {
+        COL = col_bytes(d);
+        AM1 = d.A - 1u;
+        k8 = (threadIdx.x & 15u) * 8u;
+        const uint32_t sraw = smem_u32(sm);
+        tbase = (sraw + COL - 1) / COL * COL;
+        unsigned char* base = sm + (tbase - sraw);
+        unsigned char* code_of = base + (size_t)d.A * COL;   // state -> code
+        unsigned char* state_of = code_of + 256;             // code -> state
+        cof = smem_u32(code_of);
+        sof = smem_u32(state_of);
+        // codes: non-accepting states first (in state order), accepting states last
+        uint32_t nacc = 0;
+        for (uint32_t t = 0; t < d.Qp; ++t) nacc += d.acc[t];
+        hitK = 256u - d.Qpad + nacc;   // code >= Qpad - nacc  <=>  code + hitK carries out of 8 bits
+        lgQ = d.log2Qpad;
+        for (uint32_t s = threadIdx.x; s < d.Qpad; s += blockDim.x) {
+            uint32_t code = s;
+            if (s < d.Qp) {
+                uint32_t before_same = 0;
+                const uint32_t a = d.acc[s];
+                for (uint32_t t = 0; t < s; ++t) before_same += (d.acc[t] == a);
+                code = a ? d.Qpad - nacc + before_same : before_same;
+            } else {
+                code = s - nacc;   // unused padding states fill the gap below the accepting codes
+            }
+            code_of[s] = (unsigned char)code;
+            state_of[code] = (unsigned char)s;
+        }
+        __syncthreads();
+        const uint32_t total = d.A * d.Qpad;
+        for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
+            const uint32_t s = i & (d.Qpad - 1u), c = i >> d.log2Qpad;
+            uint32_t dest;
+            if (d.lanes_u32) dest = (__ldg(reinterpret_cast<const uint32_t*>(d.lanes_tab) + (size_t)c * d.Qpad + s) & ((d.Qpad - 1u) * 4u)) >> 2;
+            else dest = (__ldg(reinterpret_cast<const uint16_t*>(d.lanes_tab) + (size_t)c * d.Qpad + s) & ((d.Qpad - 1u) * 2u)) >> 1;
+            const uint32_t cs = code_of[s], cd = code_of[dest];
+            unsigned char* row = base + (size_t)c * COL + (cs >> 3) * 128u + (cs & 7u);
+#pragma unroll 4
+            for (uint32_t kk = 0; kk < 16u; ++kk) row[kk * 8u] = (unsigned char)cd;
+        }
+    }
+    __device__ __forceinline__ uint32_t col(uint32_t c) const { return min(c, AM1) * COL + (tbase | k8); }
+    __device__ __forceinline__ uint32_t colm(uint32_t c) const { return min(c, AM1) * COL + (tbase | k8); }
+    // e = code (8 bits)
+    __device__ __forceinline__ uint32_t next(uint32_t e, uint32_t colc) const {
+        uint32_t v;
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(colc | ((e & 0xF8u) << 4) | (e & 7u)));
+        return v;
+    }
+    __device__ __forceinline__ uint32_t state(uint32_t e) const {
+        uint32_t v;
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(sof + e));
+        return v;
+    }
+    __device__ __forceinline__ uint32_t hit(uint32_t e) const { return (e + hitK) >> 8; }
+    __device__ __forceinline__ uint32_t start(uint32_t s) const {
+        uint32_t v;
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(cof + s));
+        return v;
+    }
+    __device__ __forceinline__ uint32_t word_mask() const { return 0xFFFFFFFFu; }
+};
+
 // Hybrid table for the follow walk of tables that do not fit shared memory (cfg5: 1024 x 256,
 // 512 KiB): the first CS symbol columns live in shared memory, PACKED three 10-bit states per
 // word (WPC = ceil(Qpad / 3) words per column), the other columns are read from the u16 table
@@ -277,7 +361,7 @@ __host__ __device__ __forceinline__ size_t rep_smem_bytes(const DevDfa& d, uint3
 // tools/follow_probe.cu); with 144 of 256 columns in shared memory and two chunks per
 // thread the probe reaches 1.7 (profiles/r02_follow_probe.txt).
 struct TabH {
-    static constexpr bool kSmem = true, kW32 = false, kRep = false, kHyb = true;
+    static constexpr bool kSmem = true, kW32 = false, kRep = false, kHyb = true, kByte = false;
     static constexpr uint32_t kBudget = 192u * 1024u;   // more starves the L1 the input stream needs
     const uint16_t* g;
     uint32_t sbase, abase, CS, WPC, Qpad, AM1, CMASK;
@@ -361,12 +445,12 @@ struct TabH {
 // staging and footprint of any follow table type
 template <class TT>
 __device__ __forceinline__ void tab_setup(TT& T, const DevDfa& d, unsigned char* sm) {
-    if constexpr (TT::kRep || TT::kHyb) T.init(d, sm);
+    if constexpr (TT::kRep || TT::kHyb || TT::kByte) T.init(d, sm);
     else T.init(d, stage_table<TT::kSmem, TT::kW32>(d, sm));
 }
 template <class TT>
 __host__ __device__ __forceinline__ size_t tab_smem(const DevDfa& d) {
-    if constexpr (TT::kHyb) return TT::bytes(d);
+    if constexpr (TT::kHyb || TT::kByte) return TT::bytes(d);
     else if constexpr (TT::kRep) return rep_smem_bytes(d, TT::kR);
     else return smem_tab_bytes(d, TT::kSmem);
 }
@@ -1601,7 +1685,11 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     }
     prof_after("conv_set", s);
     if constexpr (SMEM) {
-        if (plan.conv_rep == 8) e = launch_follow_cpt<TabR<8>>(plan, P, rep_smem_bytes(d, 8), s);
+        if (plan.conv_rep == 116 && TabB::applies(d)) {
+            if (!(plan.conv_tma && launch_follow_tma<TabB>(P, TabB::bytes(d), s, &e)))
+                e = launch_follow<TabB, 1>(plan, P, TabB::bytes(d), s);
+        }
+        else if (plan.conv_rep == 8) e = launch_follow_cpt<TabR<8>>(plan, P, rep_smem_bytes(d, 8), s);
         else if (plan.conv_rep == 16) e = launch_follow_cpt<TabR<16>>(plan, P, rep_smem_bytes(d, 16), s);
         else e = launch_follow_cpt<Tab<SMEM, W32>>(plan, P, tb, s);
     } else {
@@ -1656,6 +1744,7 @@ size_t conv_ws_total(uint64_t p) { return conv_ws_bytes(p); }
 
 size_t conv_rep_smem(const DevDfa& d, uint32_t R) { return rep_smem_bytes(d, R); }
 bool conv_hybrid_applies(const DevDfa& d) { return TabH::applies(d); }
+bool conv_byte_table_applies(const DevDfa& d) { return TabB::applies(d); }
 size_t conv_follow_tma_smem(size_t table_bytes) { return follow_tma_smem(table_bytes); }
 
 size_t conv_set_smem_bytes(const DevDfa& d, bool smem_tab, uint32_t cap, uint32_t warps) {

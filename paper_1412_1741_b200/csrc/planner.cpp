@@ -172,9 +172,14 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         plan->conv_tma = 0;
         plan->set_own = 1;
         if (const char* e = getenv("PAREM_CONV_TMA")) plan->conv_tma = (uint32_t)atoi(e);   // experiments
-        plan->conv_rep = 0;
+        // follow table: sixteen byte-entry copies (TabB, 116) when the DFA has <= 256 states and
+        // they fit 112 KB -- 2 wavefronts per lookup instead of ~3.6 (cfg3 follow 2.33 -> 2.10
+        // ms); else the plain table.  PAREM_CONV_REP = 0 / 8 / 16 / 116 for experiments.
+        plan->conv_rep = conv_smem_tab && conv_byte_table_applies(d) ? 116 : 0;
         if (const char* e = getenv("PAREM_CONV_REP")) plan->conv_rep = (uint32_t)atoi(e);
-        if (plan->conv_rep) {
+        if (plan->conv_rep == 116) {   // byte-entry table, 16 copies (TabB)
+            if (!conv_smem_tab || !conv_byte_table_applies(d)) plan->conv_rep = 0;
+        } else if (plan->conv_rep) {
             const size_t rb = conv_smem_tab ? conv_rep_smem(d, plan->conv_rep) : 0;
             const size_t need = plan->conv_tma ? conv_follow_tma_smem(rb) : rb;
             if (!rb || (plan->conv_rep != 8 && plan->conv_rep != 16) || need > 232448 - 1024) plan->conv_rep = 0;
