@@ -28,7 +28,7 @@ for seed in range(int(sys.argv[1]) if len(sys.argv) > 1 else 300):
                      candidates=str(rng.choice(["parem", "parem", "enum"])))
     # the converging path's opt-in variants (read by the planner on every call)
     os.environ["PAREM_CONV_TMA"] = str(int(rng.random() < 0.3))
-    os.environ["PAREM_CONV_REP"] = str(int(rng.choice([0, 0, 8, 16])))
+    os.environ["PAREM_CONV_REP"] = str(int(rng.choice([0, 8, 16, 116, 116])))   # 116: byte-entry table (the default where it applies)
     os.environ["PAREM_CONV_HYB"] = str(int(rng.random() < 0.3))   # hybrid follow table (Q <= 1024, L2 tables)
     os.environ["PAREM_CONV_CPT"] = str(int(rng.choice([1, 1, 2])))  # chunks per follow thread (interleaved walk)
     ref = oracle.walk(t, q0, acc, x)
