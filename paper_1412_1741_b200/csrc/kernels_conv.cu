@@ -1092,7 +1092,7 @@ __host__ __device__ __forceinline__ size_t follow_tma_smem(size_t tb) {
 }
 
 template <class TT>
-__global__ void __launch_bounds__(kFThreads) conv_follow_tma_kernel(const MatchParams P,
+__global__ void __launch_bounds__(kFThreads, 1) conv_follow_tma_kernel(const MatchParams P,
                                                                     const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(16) unsigned char sm[];
     const DevDfa& d = P.d;
