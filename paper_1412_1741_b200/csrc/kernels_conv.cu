@@ -1091,7 +1091,11 @@ __host__ __device__ __forceinline__ size_t follow_tma_smem(size_t tb) {
     return ((tb + 1023) & ~(size_t)1023) + (kFThreads / 32) * (kFStages * kFStageBytes + 8 * kFStages) + 1024;
 }
 
-template <class TT>
+// COOP = true replaces the TMA engine by warp-cooperative cp.async copies on the LSU path
+// (lane l copies 16-byte unit l & 3 of rows 8 i + (l >> 2), i = 0..3, into the same 64B-swizzled
+// stage layout): a stream of 32-row x 64-byte boxes is bound by the TMA engine's per-row rate
+// (profiles/r02_conv_sweeps.txt), while four cp.async instructions touch 8 lines each.
+template <class TT, bool COOP>
 __global__ void __launch_bounds__(kFThreads, 1) conv_follow_tma_kernel(const MatchParams P,
                                                                     const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -1138,7 +1142,25 @@ __global__ void __launch_bounds__(kFThreads, 1) conv_follow_tma_kernel(const Mat
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s_lo = min(s_lo, __shfl_xor_sync(0xFFFFFFFFu, s_lo, o));
     const bool warp_staged = s_lo < nst;
-    if (lane == 0 && warp_staged) {
+    // cooperative copy of box sb of this warp's 32 rows into stage buffer `buf` (one commit group)
+    auto coop_issue = [&](uint32_t sb, uint32_t buf) {
+        if (sb < nst) {
+#pragma unroll
+            for (uint32_t i = 0; i < 4; ++i) {
+                const uint32_t r = 8u * i + (lane >> 2), u = lane & 3u;
+                if (row0 + r < pfull) {
+                    const uint8_t* src = in + (row0 + r) * P.L + (uint64_t)sb * kFBox + 16u * u;
+                    const uint32_t dst = buf + r * kFBox + ((u ^ ((r >> 1) & 3u)) << 4);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+                }
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if constexpr (COOP) {
+        if (warp_staged)
+            for (uint32_t k = 0; k < kFStages; ++k) coop_issue(s_lo + k, stage0 + k * kFStageBytes);
+    } else if (lane == 0 && warp_staged) {
         for (uint32_t k = 0; k < kFStages; ++k) mbar_init(mbar0 + 8 * k, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (uint32_t k = 0; k < kFStages && s_lo + k < nst; ++k) {
@@ -1158,7 +1180,14 @@ __global__ void __launch_bounds__(kFThreads, 1) conv_follow_tma_kernel(const Mat
         const uint32_t sw = (lane >> 1) & 3u, off = lane * kFBox;
         uint32_t slot = 0, phase = 0;
         for (uint32_t s = s_lo; s < nst; ++s) {
-            mbar_wait(mbar0 + 8 * slot, phase);
+            if constexpr (COOP) {
+                // the oldest group (this slot's) is complete for this lane's copies; the warp
+                // barrier makes every lane's copies visible
+                asm volatile("cp.async.wait_group %0;" ::"n"(kFStages - 1) : "memory");
+                __syncwarp();
+            } else {
+                mbar_wait(mbar0 + 8 * slot, phase);
+            }
             const uint32_t buf = stage0 + slot * kFStageBytes;
             uint4 x[4];
 #pragma unroll
@@ -1181,7 +1210,9 @@ __global__ void __launch_bounds__(kFThreads, 1) conv_follow_tma_kernel(const Mat
             // refill this slot only after every lane consumed its staged words (the TMA
             // write must not overtake an in-flight shared load of the same buffer)
             __syncwarp();
-            if (lane == 0 && s + kFStages < nst) {
+            if constexpr (COOP) {
+                coop_issue(s + kFStages, buf);   // always commits, so the group count stays in step
+            } else if (lane == 0 && s + kFStages < nst) {
                 mbar_expect_tx(mbar0 + 8 * slot, kFStageBytes);
                 tma_load_2d(buf, &tmap, (int32_t)((s + kFStages) * kFBox), (int32_t)row0, mbar0 + 8 * slot);
             }
@@ -1195,8 +1226,25 @@ __global__ void __launch_bounds__(kFThreads, 1) conv_follow_tma_kernel(const Mat
             }
         }
     }
-    if (act && !staged) {   // the last chunk: from global memory, every route
-        for (uint64_t a = b0 + m; a < b1; ++a) F.step1(0, in[a]);
+    {
+        // The last chunk is not a full row: its lane walks it with the thread-stream loop
+        // (16-byte vectors, prefetch ring).  A byte-at-a-time walk of up to L bytes by ONE
+        // thread took longer than the whole staged part (3 ms for a 56 KB chunk) and was
+        // what made every staged variant look slow until round 2's last session.
+        const bool lastc = act && !staged;
+        uint64_t a = b0 + m;
+        if (lastc) {
+            const uint64_t mis = (uint64_t)(((uintptr_t)(in + a)) & 15u);
+            uint64_t hd = mis ? a + (16 - mis) : a;
+            if (hd > b1) hd = b1;
+            for (; a < hd; ++a) F.step1(0, in[a]);
+        }
+        F.nv[0] = lastc ? (uint32_t)((b1 - a) >> 4) : 0u;
+        F.p[0] = in + a;
+        const uint32_t nvl = __reduce_max_sync(0xFFFFFFFFu, F.nv[0]);
+        if (nvl) F.run(nvl, true);   // warp-uniform call; lanes without vectors idle
+        if (lastc)
+            for (a += (uint64_t)F.nv[0] << 4; a < b1; ++a) F.step1(0, in[a]);
     }
     {
         // staged rows: head = bytes up to the first staged 16-byte unit
@@ -1637,12 +1685,13 @@ cudaError_t launch_follow(const Plan& plan, const MatchParams& P, size_t smem, c
 // TMA-staged follow when the input is 16-byte aligned and rows are whole boxes; false =
 // not applicable (the caller uses the thread-stream follow)
 template <class TT>
-bool launch_follow_tma(const MatchParams& P, size_t tb, cudaStream_t s, cudaError_t* err) {
+bool launch_follow_tma(const MatchParams& P, size_t tb, cudaStream_t s, cudaError_t* err, bool coop = false) {
     if ((((uintptr_t)P.in) & 15u) || P.L % kFBox || P.L < kFBox || P.p < 2) return false;
     CUtensorMap map;
     memset(&map, 0, sizeof(map));
-    if (!encode_rows_map(&map, P.in, P.L, P.p - 1, kFBox, 32)) return false;
-    const void* fn = reinterpret_cast<const void*>(&conv_follow_tma_kernel<TT>);
+    if (!coop && !encode_rows_map(&map, P.in, P.L, P.p - 1, kFBox, 32)) return false;
+    const void* fn = coop ? reinterpret_cast<const void*>(&conv_follow_tma_kernel<TT, true>)
+                          : reinterpret_cast<const void*>(&conv_follow_tma_kernel<TT, false>);
     cudaError_t e = smem_optin(fn, follow_tma_smem(tb));   // tb = the table type's footprint
     if (e == cudaSuccess) {
         void* args[] = {const_cast<MatchParams*>(&P), &map};
@@ -1656,7 +1705,7 @@ bool launch_follow_tma(const MatchParams& P, size_t tb, cudaStream_t s, cudaErro
 template <class TT>
 cudaError_t launch_follow_cpt(const Plan& plan, const MatchParams& P, size_t smem, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
-    if (plan.conv_tma && launch_follow_tma<TT>(P, smem, s, &e)) return e;
+    if (plan.conv_tma && launch_follow_tma<TT>(P, smem, s, &e, plan.conv_tma == 2)) return e;
     return plan.conv_cpt == 2 ? launch_follow<TT, 2>(plan, P, smem, s) : launch_follow<TT, 1>(plan, P, smem, s);
 }
 
@@ -1685,13 +1734,25 @@ int launch_conv_t(const Plan& plan, const MatchParams& P, cudaStream_t s) {
     }
     prof_after("conv_set", s);
     if constexpr (SMEM) {
-        if (plan.conv_rep == 116 && TabB::applies(d)) {
-            if (!(plan.conv_tma && launch_follow_tma<TabB>(P, TabB::bytes(d), s, &e)))
-                e = launch_follow<TabB, 1>(plan, P, TabB::bytes(d), s);
+        // staged follow (TMA or cooperative cp.async) when the input allows it, else the
+        // thread-stream follow -- with the byte-entry table where it applies (the
+        // bank-confined u16 copies starve the thread streams' L1)
+        const bool coop = plan.conv_tma == 2;
+        bool done = false;
+        if (plan.conv_tma) {
+            if (plan.conv_rep == 8) done = launch_follow_tma<TabR<8>>(P, rep_smem_bytes(d, 8), s, &e, coop);
+            else if (plan.conv_rep == 16) done = launch_follow_tma<TabR<16>>(P, rep_smem_bytes(d, 16), s, &e, coop);
+            else if (plan.conv_rep == 116 && TabB::applies(d)) done = launch_follow_tma<TabB>(P, TabB::bytes(d), s, &e, coop);
+            else done = launch_follow_tma<Tab<SMEM, W32>>(P, tb, s, &e, coop);
         }
-        else if (plan.conv_rep == 8) e = launch_follow_cpt<TabR<8>>(plan, P, rep_smem_bytes(d, 8), s);
-        else if (plan.conv_rep == 16) e = launch_follow_cpt<TabR<16>>(plan, P, rep_smem_bytes(d, 16), s);
-        else e = launch_follow_cpt<Tab<SMEM, W32>>(plan, P, tb, s);
+        if (!done) {
+            const bool byte_tab = TabB::applies(d) && (plan.conv_rep == 116 || (plan.conv_tma && plan.conv_rep != 0));
+            if (byte_tab) e = launch_follow<TabB, 1>(plan, P, TabB::bytes(d), s);
+            else if (plan.conv_rep == 8 && !plan.conv_tma) e = launch_follow<TabR<8>, 1>(plan, P, rep_smem_bytes(d, 8), s);
+            else if (plan.conv_rep == 16 && !plan.conv_tma) e = launch_follow<TabR<16>, 1>(plan, P, rep_smem_bytes(d, 16), s);
+            else e = plan.conv_cpt == 2 ? launch_follow<Tab<SMEM, W32>, 2>(plan, P, tb, s)
+                                        : launch_follow<Tab<SMEM, W32>, 1>(plan, P, tb, s);
+        }
     } else {
         if (plan.conv_hyb && !W32 && TabH::applies(d))
             e = plan.conv_cpt == 2 ? launch_follow<TabH, 2>(plan, P, TabH::bytes(d), s)

@@ -169,13 +169,23 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         // follow (conv_tma) is faster per byte on shared-memory tables but needs ~1024
         // chains per SM; at that chunk count the set walk costs more than it saves (cfg3:
         // 3.13 ms vs 2.95 ms per step, profiles/r02_conv_sweeps.txt), so it is opt-in.
-        plan->conv_tma = 0;
+        // Shared-memory tables: the staged follow (rows streamed through shared memory by TMA; 2 =
+        // by warp-cooperative cp.async) with the follow table in 8 bank-confined copies
+        // (TabR<8>) at 512 chains per SM -- cfg3 follow 1.80 ms against 2.10 ms for the
+        // thread-stream follow with the byte-entry table (which stays the fallback when the
+        // input is not 16-byte aligned or a chunk length is forced).  The staged follow only
+        // became the faster one once the last chunk was kept short (below).
+        plan->conv_tma = conv_smem_tab ? 1 : 0;
         plan->set_own = 1;
         if (const char* e = getenv("PAREM_CONV_TMA")) plan->conv_tma = (uint32_t)atoi(e);   // experiments
         // follow table: sixteen byte-entry copies (TabB, 116) when the DFA has <= 256 states and
         // they fit 112 KB -- 2 wavefronts per lookup instead of ~3.6 (cfg3 follow 2.33 -> 2.10
         // ms); else the plain table.  PAREM_CONV_REP = 0 / 8 / 16 / 116 for experiments.
         plan->conv_rep = conv_smem_tab && conv_byte_table_applies(d) ? 116 : 0;
+        if (plan->conv_tma && conv_smem_tab) {
+            const size_t rb = conv_rep_smem(d, 8);
+            if (rb && conv_follow_tma_smem(rb) <= 232448 - 1024) plan->conv_rep = 8;
+        }
         if (const char* e = getenv("PAREM_CONV_REP")) plan->conv_rep = (uint32_t)atoi(e);
         if (plan->conv_rep == 116) {   // byte-entry table, 16 copies (TabB)
             if (!conv_smem_tab || !conv_byte_table_applies(d)) plan->conv_rep = 0;
@@ -214,7 +224,7 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
             const double rho = L512 > 0 ? (double)dfa->conv_work4 / L512 : 0.0;
             plan->conv_fthreads = rho >= 1.5 ? 320 : rho >= 0.75 ? 416 : 512;
         }
-        uint64_t chains = (uint64_t)sms * (plan->conv_tma ? 1024 : plan->conv_fthreads * plan->conv_cpt);
+        uint64_t chains = (uint64_t)sms * (plan->conv_tma ? 512 : plan->conv_fthreads * plan->conv_cpt);
         uint32_t dmax = 4;
         uint64_t headx = 16;
         if (const char* e = getenv("PAREM_CONV_CHAINS")) chains = strtoull(e, nullptr, 10);   // experiments
@@ -232,6 +242,16 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
             if (plan->conv_tma) {
                 L = (L + 63) & ~63ull;
                 if (L % 256 == 0) L += 64;
+                // The last chunk (n mod L bytes, not a full row) is walked by one lane after its
+                // warp's staged rows: keep it short -- among the next row lengths take the one
+                // with the smallest remainder (a 36 KB last chunk cost cfg3 ~1 ms of 2.9).
+                uint64_t bestL = L, bestr = n % L ? n % L : L;
+                for (uint64_t c = L; c < L + 64 * 96 && bestr > 2048; c += 64) {
+                    if (c % 256 == 0) continue;
+                    const uint64_t r = n % c ? n % c : c;
+                    if (r < bestr) { bestr = r; bestL = c; }
+                }
+                L = bestL;
             } else {
                 L = (L + 15) & ~15ull;
                 // thread-per-chunk 16-B load streams at a stride that is a multiple of 128 B
