@@ -164,11 +164,9 @@ int make_plan(const parem_dfa* dfa, uint64_t n, const parem_options* opts, Plan*
         // With the opt-in TMA-staged follow the rows are whole 64-byte boxes (and not
         // multiples of 256 B: TMA row streams at such strides are slower,
         // profiles/r01_stride_probe.txt).
-        // Follow input: each thread streams its row with 16-byte loads that do not allocate
-        // in L1 (an L2-resident table keeps the whole L1: carveout 0).  The TMA-staged
-        // follow (conv_tma) is faster per byte on shared-memory tables but needs ~1024
-        // chains per SM; at that chunk count the set walk costs more than it saves (cfg3:
-        // 3.13 ms vs 2.95 ms per step, profiles/r02_conv_sweeps.txt), so it is opt-in.
+        // L2-resident tables: each thread streams its row with 16-byte loads that do not
+        // allocate in L1 (the table keeps the whole L1: carveout 0); the staged follow is
+        // slower there (cfg5 18.8 vs 14.2 ms, cfg4 14.0 vs 11.3 ms).
         // Shared-memory tables: the staged follow (rows streamed through shared memory by TMA; 2 =
         // by warp-cooperative cp.async) with the follow table in 8 bank-confined copies
         // (TabR<8>) at 512 chains per SM -- cfg3 follow 1.80 ms against 2.10 ms for the
