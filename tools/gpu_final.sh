@@ -18,7 +18,7 @@ for k in 3 4 5; do
   $B > $F/plain1_$k.json 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"conv_set|conv_follow" -s 6 -c 2 -o $F/prof_cfg$k $B > $F/ncu_full_$k.log 2>&1
   for kn in conv_set conv_follow; do
-    python tools/ncu_json.py $F/prof_cfg$k.ncu-rep "${kn}_kernel" $F/r02_ncu_full_cfg${k}_${kn}.json "tools/gpu_final.sh: ncu --set full --clock-control none, bench.py --config $k --quick --steps 1 (round-2 final code)" > /dev/null 2>&1
+    python tools/ncu_json.py $F/prof_cfg$k.ncu-rep "${kn}" $F/r02_ncu_full_cfg${k}_${kn}.json "tools/gpu_final.sh: ncu --set full --clock-control none, bench.py --config $k --quick --steps 1 (round-2 final code)" > /dev/null 2>&1
   done
   rm -f $F/prof_cfg$k.ncu-rep
 done
